@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""Benchmark driver (one JSON line on rank 0).
+
+Headline (``--workload pr_s24``, default): PageRank, 20 fixed fp64
+iterations, damping 0.85, on the BASELINE R-MAT graph (a=.57 b=c=.19,
+edge factor 16, seed 1) at scale 24 — configs[1]'s algorithm at the scale
+where BASELINE.json's north_star states the HBM-roofline target (the s20
+graph of configs[1] is ~L2-sized).  One step = one full ``pagerank`` call
+(20 pull iterations) on a device-resident CSR; value = GTEPS = 20*m / t.
+
+The same line carries ``workloads`` with every other BASELINE config
+(configs[0] BFS s16, configs[1] PR s20, configs[2] DO-BFS + CC s24,
+configs[3] TC s20, configs[4] batch updates on the blocked container at
+s22), ``roofline`` for the PageRank pull kernel, ``e2e`` through the C ABI
+with host buffers, and ``cpu_baseline`` (the reference library itself,
+oracle/_ref/libgbref.so, on this host's cores).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: one process per GPU (torchrun); the path does not shard in this
+tier, so every rank runs an independent replica (weak scaling), timed as
+the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+RMAT = (0.57, 0.19, 0.19)
+TINY = float(np.finfo(np.float64).tiny)
+METRIC = "PageRank GTEPS (20 fixed fp64 iterations, 20*m/t)"
+UNIT = "GTEPS"
+L2_BYTES = 126 * 2**20
+
+
+# ---------------------------------------------------------------- plumbing
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if os.environ.get("GBG_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
+        dist.init_process_group(backend=backend)
+    return rank, local, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def events_time(torch, stream_ptr: int, fn, steps: int) -> float:
+    """Seconds for `steps` calls of fn, CUDA events on the library's stream."""
+    s = torch.cuda.ExternalStream(stream_ptr)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(steps):
+        fn()
+    e1.record(s)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def pr_bytes(n: int, m: int, w: int = 8) -> int:
+    """B_PR = W(n+1) + 4m + 16n per iteration (offsets, ids,
+    one fp64 read + one fp64 write per vertex)."""
+    return w * (n + 1) + 4 * m + 16 * n
+
+
+def bfs_model_bytes(n, off, depth, modes, sizes, degsums, w=8):
+    """SURVEY §8(d) BFS byte model using the modes actually chosen (dense
+    E_scan approximated by the degree of the scanned vertices' prefix is not
+    recomputed here: dense levels count W(n+1) + 3 bm + 4 |N| + 4 E_scan with
+    E_scan <= sum of scanned degrees; we report the lower bound without
+    E_scan)."""
+    bm = (n + 7) // 8
+    total = 0
+    for i, md in enumerate(modes):
+        f = sizes[i]
+        nxt = sizes[i + 1] if i + 1 < len(sizes) else 0
+        if md == 0:
+            total += 4 * f + 2 * w * f + 4 * degsums[i] + 8 * nxt + bm
+        else:
+            total += w * (n + 1) + 3 * bm + 4 * nxt
+    return total
+
+
+# ---------------------------------------------------------------- workloads
+def run_pagerank(torch, gbg, g, steps, warmup, iters=20):
+    n, m = g.num_vertices(), g.num_edges()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    step = lambda: gbg.pagerank_device(g, out.data_ptr(), 0.85, iters, TINY)  # noqa: E731
+    for _ in range(warmup):
+        step()
+    l0 = g.launch_count()
+    t = events_time(torch, g.stream(), step, steps)
+    launches = g.launch_count() - l0
+    return t / steps, launches, out
+
+
+def run_bfs(torch, gbg, g, src, steps, warmup):
+    depth = torch.empty(g.num_vertices(), dtype=torch.int32, device="cuda")
+    stats = {}
+
+    def step():
+        stats.update(gbg.bfs_device(g, src, depth.data_ptr()))
+
+    for _ in range(warmup):
+        step()
+    t = events_time(torch, g.stream(), step, steps)
+    return t / steps, stats, depth
+
+
+def run_updates(torch, gbg, S, steps, warmup, sizes):
+    """configs[4]: blocked container at scale S; per size, a base-disjoint
+    batch (filter untimed, bench.cpp:150-169) inserted (timed: device
+    prepare = sort + dedup, then merge), BFS from the max-degree vertex,
+    deleted (timed).  Throughput = sampled batch size / seconds
+    (bench.hpp:72-74).  Batches are device-resident before timing."""
+    g = gbg.generate_rmat(S, 16 << S, 1, *RMAT, kind=gbg.KIND_BLOCKED)
+    off, nbr = g.to_csr()
+    n = g.num_vertices()
+    src_of = np.repeat(np.arange(n, dtype=np.uint64), np.diff(off.astype(np.int64)))
+    base_keys = (src_of << np.uint64(32)) | nbr.astype(np.uint64)
+    del src_of
+    res = {}
+    for size in sizes:
+        buf = torch.empty(4 * size, dtype=torch.int32, device="cuda")
+        seed = _hash_combine(_hash_combine(2, size), 0)
+        gbg.generate_update_batch_device(S, size, seed, buf.data_ptr(), *RMAT)
+        raw = buf.cpu().numpy().view(np.uint32).reshape(-1, 2)
+        keys = (raw[:, 0].astype(np.uint64) << np.uint64(32)) | raw[:, 1].astype(np.uint64)
+        fresh = np.ascontiguousarray(raw[~np.isin(keys, base_keys)])
+        dev = torch.from_numpy(fresh.view(np.int32)).cuda()
+        cnt = fresh.shape[0]
+        ins_t, del_t, bfs_t, applied = [], [], [], 0
+        src = int(np.argmax(np.diff(off.astype(np.int64))))
+        for rep in range(warmup + steps):
+            ti = events_time(torch, g.stream(), lambda: res.__setitem__("_a", g.insert_batch_device(dev.data_ptr(), cnt)), 1)
+            applied = res.pop("_a")
+            depth = torch.empty(n, dtype=torch.int32, device="cuda")
+            tb = events_time(torch, g.stream(), lambda: gbg.bfs_device(g, src, depth.data_ptr()), 1)
+            td = events_time(torch, g.stream(), lambda: g.delete_batch_device(dev.data_ptr(), cnt), 1)
+            if rep >= warmup:
+                ins_t.append(ti)
+                del_t.append(td)
+                bfs_t.append(tb)
+        ti, td = statistics.median(ins_t), statistics.median(del_t)
+        res[str(size)] = {"insert_edges_per_s": size / ti, "delete_edges_per_s": size / td,
+                          "insert_ms": ti * 1e3, "delete_ms": td * 1e3, "bfs_after_insert_ms": statistics.median(bfs_t) * 1e3,
+                          "raw_arcs": 2 * size, "fresh_arcs": cnt, "applied_arcs": applied,
+                          "applied_arcs_per_s": applied / ti}
+    return res, g
+
+
+def _mix64(x):
+    M = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+def _hash_combine(a, b):
+    M = (1 << 64) - 1
+    return _mix64(a ^ ((b + 0x9E3779B97F4A7C15 + (a << 6) + (a >> 2)) & M))
+
+
+# ---------------------------------------------------------------- CPU (reference library)
+def cpu_reference_pr(off, nbr, n, steps, warmup, iters=1):
+    """The UNMODIFIED reference CPU path (gb::pagerank over gb::CsrGraph,
+    compiled from /root/reference into oracle/_ref/libgbref.so) with all
+    host threads; a bounded sample: `iters` of the 20 iterations per step."""
+    from oracle.bindings import Ref
+
+    ref = Ref()
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    t0 = time.perf_counter()
+    g = ref.csr(n, off, nbr)
+    build_s = time.perf_counter() - t0
+    for _ in range(warmup):
+        g.pagerank(0.85, iters, TINY)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        g.pagerank(0.85, iters, TINY)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    m = int(off[n])
+    return {"value": iters * m / t / 1e9, "unit": UNIT, "cores": ref.num_threads(), "kind": "reference",
+            "sample": f"{iters} of the 20 PageRank iterations per step over the full scale-24 graph "
+                      f"(m={m}), median of {steps} step(s) after {warmup} warm-up; "
+                      f"reference gb::pagerank via oracle/_ref/libgbref.so, OMP threads={threads}",
+            "seconds_per_step": t, "container_build_s": build_s}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, local, world = dist_setup()
+
+    import torch
+
+    torch.cuda.set_device(local)
+    import paper_2405_11671_b200.graph as gbg
+
+    gbg.set_device(local)
+    S = args.scale
+    config = {"workload": f"pagerank_rmat_s{S}", "graph": f"R-MAT scale {S}, edge factor 16, a=.57 b=c=.19, seed 1, "
+              "symmetrized, self-loops/duplicates removed (device generator, bit-exact with gb::generate_rmat)",
+              "iterations": 20, "damping": 0.85, "container": "csr (uint64 offsets, uint32 ids)",
+              "l2_policy": "inputs larger than L2 (2.2 GB CSR vs 126 MB L2); no flush",
+              "parallelism": f"replicas x{world}"}
+
+    if args.impl == "reference":
+        # reference arm: rank 0 times the reference CPU path; others exit
+        if rank != 0:
+            barrier(world)
+            return
+        g = gbg.generate_rmat(S, 16 << S, 1, *RMAT)
+        off, nbr = g.to_csr()
+        n = g.num_vertices()
+        del g
+        cb = cpu_reference_pr(off, nbr, n, args.steps, args.warmup)
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": dict(config, sample=cb["sample"]),
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "host_cpu": cpu_model()}
+        print(json.dumps(line), flush=True)
+        barrier(world)
+        return
+
+    # ---- headline: PageRank on the device CSR
+    g = gbg.generate_rmat(S, 16 << S, 1, *RMAT)
+    n, m = g.num_vertices(), g.num_edges()
+    barrier(world)
+    with Clocks(local) as clk:
+        t_step, launches, pr_out = run_pagerank(torch, gbg, g, args.steps, args.warmup)
+    t_max = max_over_ranks(t_step, world, device="cuda")
+    value = world * 20 * m / t_max / 1e9
+    peaks, peak_src = measured_peaks()
+    it_s = t_step / 20
+    achieved = pr_bytes(n, m) / it_s / 1e9
+    traffic = ncu_traffic("pr_iter_k")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "kernel": "pr_iter_k (one fused pull iteration)",
+                "algorithmic_bytes_per_launch": pr_bytes(n, m), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                "launch_seconds": it_s, "note": "launch time = whole pagerank call / 20 (includes init + readback)"}
+
+    # ---- e2e through the C ABI with host buffers: pinned CSR upload,
+    # 20 iterations, ranks read back to host, every step
+    off, nbr = g.to_csr()
+    off_p = torch.from_numpy(off.view(np.int64)).pin_memory()
+    nbr_p = torch.from_numpy(nbr.view(np.int32)).pin_memory()
+    off_h = off_p.numpy().view(np.uint64)
+    nbr_h = nbr_p.numpy().view(np.uint32)
+
+    def e2e_step():
+        h = gbg.CsrGraph.from_csr(off_h, nbr_h)
+        gbg.pagerank(h, 0.85, 20, TINY)
+        del h
+
+    e2e_step()
+    barrier(world)
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_e2e = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world, device="cuda")
+    e2e = {"value": world * 20 * m / t_e2e / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": int(off.nbytes + nbr.nbytes), "d2h_bytes_per_step": 8 * n,
+           "ms_per_step": t_e2e * 1e3,
+           "path": "gbg_csr_create (pinned host CSR -> device, validated) + gbg_pagerank (ranks -> host)"}
+
+    workloads = {}
+    if rank == 0 and not args.no_secondary:
+        # configs[2]: DO-BFS + CC on the same scale-24 graph
+        src = int(np.argmax(np.diff(off.astype(np.int64))))
+        tb, st, depth = run_bfs(torch, gbg, g, src, args.steps, args.warmup)
+        d = depth.cpu().numpy()
+        deg = np.diff(off.astype(np.int64))
+        g500 = int(deg[d >= 0].sum() // 2)
+        workloads[f"bfs_s{S}"] = {"ms": tb * 1e3, "gteps_graph500": g500 / tb / 1e9, "arcs_per_s": m / tb,
+                                  "modes": st["modes"], "frontier_sizes": st["frontier_sizes"],
+                                  "reached": st["reached"], "source": src,
+                                  "model_bytes_lower_bound": bfs_model_bytes(n, off, d, st["modes"],
+                                                                             st["frontier_sizes"], st["degree_sums"])}
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        for _ in range(args.warmup):
+            gbg.cc_device(g, lab.data_ptr())
+        tc_ = events_time(torch, g.stream(), lambda: gbg.cc_device(g, lab.data_ptr()), args.steps) / args.steps
+        workloads[f"cc_s{S}"] = {"ms": tc_ * 1e3, "arcs_per_s": m / tc_,
+                                 "components": int(np.unique(lab.cpu().numpy()).size)}
+    del pr_out
+    if rank == 0 and not args.no_secondary:
+        # configs[1] exactly: PR s20; configs[3]: TC s20; configs[0]: BFS s16
+        g20 = gbg.generate_rmat(20, 16 << 20, 1, *RMAT)
+        m20 = g20.num_edges()
+        t20, _, _ = run_pagerank(torch, gbg, g20, args.steps, args.warmup)
+        workloads["pr_s20"] = {"gteps": 20 * m20 / t20 / 1e9, "ms": t20 * 1e3,
+                               "note": "~L2-resident graph (134 MB CSR vs 126 MB L2)"}
+        for _ in range(1):
+            gbg.triangle_count(g20)
+        t0 = time.perf_counter()
+        tri = gbg.triangle_count(g20)
+        ttc = time.perf_counter() - t0
+        workloads["tc_s20"] = {"ms": ttc * 1e3, "triangles": tri}
+        del g20
+        g16 = gbg.generate_rmat(16, 16 << 16, 1, *RMAT)
+        o16, _ = g16.to_csr()
+        s16 = int(np.argmax(np.diff(o16.astype(np.int64))))
+        t16, st16, d16 = run_bfs(torch, gbg, g16, s16, args.steps * 4, args.warmup)
+        dd = d16.cpu().numpy()
+        e16 = int(np.diff(o16.astype(np.int64))[dd >= 0].sum() // 2)
+        workloads["bfs_s16"] = {"ms": t16 * 1e3, "gteps_graph500": e16 / t16 / 1e9, "modes": st16["modes"]}
+        del g16
+        # configs[4]: updates on the blocked container at s22
+        upd, _gb = run_updates(torch, gbg, 22, max(1, min(args.steps, 3)), 1, [10**4, 10**5, 10**6, 10**7])
+        workloads["updates_s22"] = upd
+        del _gb
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cb = cpu_reference_pr(off, nbr, n, 1, 0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (device R-MAT, bit-exact with the reference generator)",
+                "config": config, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roofline,
+                "e2e": e2e, "cpu_baseline": cpu, "workloads": workloads, "host_cpu": cpu_model(),
+                "graph": {"n": n, "m": m}}
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+if __name__ == "__main__":
+    main()

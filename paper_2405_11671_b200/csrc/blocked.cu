@@ -1,0 +1,516 @@
+// The dynamic blocked sorted-adjacency container and its batch update path.
+//
+// Reference: SetGraph<ChunkedSortedSet> with inline_k = 0 ("chunked_set",
+// registry.cpp:136-137; set_graph.hpp:26-249; neighbor_sets.hpp:259-442)
+// fed by prepare(GlobalSort) + apply_insert / apply_delete (batch.cpp:30-126).
+//
+// Layout (device): vertex v owns one allocation of cap[v] uint32 ids at
+// pool[start[v]]; its deg[v] live neighbours are the ascending prefix.
+// Capacities come in 16-byte blocks: power-of-two classes of 4..128 ids,
+// then multiples of 128 ids (512 B) with 1/8 slack — the GPU analogue of
+// ChunkedSortedSet's 128-id chunks refilled at half capacity
+// (neighbor_sets.hpp:427-438), but contiguous per vertex so every traversal
+// kernel reads a vertex's list with coalesced loads.  Allocations come from
+// a bump pointer; when the pool runs out the live lists are compacted into a
+// fresh, larger pool.
+//
+// Batch path (all on the device, starting from raw arcs):
+//   1. key = src<<L | dst, self-loops -> sentinel; range check
+//   2. radix sort (2L bits)                      prepare: sort   (batch.cpp:38)
+//   3. unique, drop self-loops                   prepare: unique (batch.cpp:37-39)
+//   4. per arc: binary search in src's list -> present?  keep the arcs that
+//      change the container (new for insert, present for delete): the
+//      applied count of insert_batch / delete_batch (neighbor_sets.hpp:339-366)
+//   5. group by source; allocate grown lists (scan + bump)
+//   6. stage touched lists, then merge (insert) / set-difference (delete)
+//      element-parallel: each element's output slot = its rank in its own
+//      list plus its rank in the other (binary search)
+//   7. deg / start / cap / m updated (MetadataTracker::add_degree/add_total,
+//      metadata.hpp:38-50)
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "keys.cuh"
+
+namespace gbg {
+
+__host__ __device__ __forceinline__ uint32_t cap_for(uint32_t d) {
+  if (d == 0) return 0;
+  if (d <= 128) {
+    uint32_t c = 4;
+    while (c < d) c <<= 1;
+    return c;
+  }
+  uint64_t want = static_cast<uint64_t>(d) + d / 8;
+  return static_cast<uint32_t>((want + 127) / 128 * 128);
+}
+
+// ---------------------------------------------------------------- build
+struct CsrDegIn {
+  const uint64_t* off;
+  __device__ __forceinline__ uint64_t operator()(uint64_t v) const { return off[v + 1] - off[v]; }
+};
+struct CapIn {
+  const uint32_t* deg;
+  __device__ __forceinline__ uint64_t operator()(uint64_t v) const { return cap_for(deg[v]); }
+};
+
+__global__ void deg_cap_from_csr_k(uint64_t n, const uint64_t* off, uint32_t* deg, uint32_t* cap) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    uint32_t d = static_cast<uint32_t>(off[v + 1] - off[v]);
+    deg[v] = d;
+    cap[v] = cap_for(d);
+  }
+}
+
+// warp per vertex copy of live lists between two layouts
+__global__ void copy_lists_k(uint64_t n, const uint64_t* src_start, const uint32_t* src, const uint32_t* deg,
+                             const uint64_t* dst_start, uint32_t* dst) {
+  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t v = w0; v < n; v += nw) {
+    const uint32_t d = deg[v];
+    const uint32_t* s = src + src_start[v];
+    uint32_t* t = dst + dst_start[v];
+    for (uint32_t j = lane; j < d; j += 32) t[j] = s[j];
+  }
+}
+
+// Lay the live lists out afresh, each vertex at cap[v] ids (caps set by the
+// caller), in a pool with room for `extra` more ids plus 50% slack.  Used at
+// build (source = a packed CSR) and when the bump pool runs out (source =
+// the current pool, which is then freed).
+void blocked_relayout(gbg_graph* g, const uint64_t* src_start, const uint32_t* src_pool, uint64_t extra,
+                      bool own_src) {
+  const uint64_t n = g->n;
+  uint64_t* nstart = dalloc<uint64_t>(n + 1);
+  device_scan<uint64_t>(g, CapIn{g->bcap}, ArrayOut<uint64_t>{nstart}, n, nstart + n, "blk.relayout");
+  uint64_t live = 0;
+  read_scalars(g, nstart + n, sizeof(live), &live);
+  uint64_t cap = live + extra + live / 2 + (uint64_t{1} << 20);
+  cap = (cap + 3) / 4 * 4;
+  uint32_t* npool = dalloc<uint32_t>(cap);
+  if (n)
+    GBG_LAUNCH(g, copy_lists_k, grid_for(n * 32, 256, g->sm_count * 64), 256, 0, n, src_start, src_pool, g->bdeg,
+               nstart, npool);
+  GBG_CUDA(cudaStreamSynchronize(g->stream));
+  if (own_src) {
+    dfree(g->bstart);
+    dfree(g->pool);
+  }
+  g->bstart = nstart;
+  g->pool = npool;
+  g->pool_cap = cap;
+  g->pool_top = live;
+  g->pool_live = live;
+}
+
+void blocked_from_device_csr(gbg_graph* g, uint64_t n, const uint64_t* off, const uint32_t* nbr) {
+  g->bdeg = dalloc<uint32_t>(n + 1);
+  g->bcap = dalloc<uint32_t>(n + 1);
+  if (n) GBG_LAUNCH(g, deg_cap_from_csr_k, grid_for(n, 256), 256, 0, n, off, g->bdeg, g->bcap);
+  // the CSR offsets double as the source "start" array of a packed layout
+  blocked_relayout(g, off, nbr, 0, false);
+}
+
+struct DegIn {
+  const uint32_t* deg;
+  __device__ __forceinline__ uint64_t operator()(uint64_t v) const { return deg[v]; }
+};
+
+const uint64_t* virtual_offsets(gbg_graph* g) {
+  if (g->kind == GBG_KIND_CSR) return g->off;
+  if (!g->voff) g->voff = dalloc<uint64_t>(g->n + 1);
+  if (!g->voff_valid) {
+    device_scan<uint64_t>(g, DegIn{g->bdeg}, ArrayOut<uint64_t>{g->voff}, g->n, g->voff + g->n, "blk.voff");
+    g->voff_valid = true;
+  }
+  return g->voff;
+}
+
+// ---------------------------------------------------------------- updates
+__global__ void make_keys_k(const uint32_t* pairs, uint64_t count, uint64_t n, BatchKeys bk, uint64_t* keys,
+                            int* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint32_t s = pairs[2 * i], d = pairs[2 * i + 1];
+    if (s >= n || d >= n) *bad = 1;
+    // self-loops become the all-ones key, itself a self-loop, dropped below
+    keys[i] = s == d ? bk.loop_key() : bk.make(s, d);
+  }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t len, uint32_t x) {
+  uint32_t lo = 0, hi = len;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// presence of each prepared arc in the container; keep those that change it
+struct ApplyIn {
+  const uint64_t* k;
+  BatchKeys bk;
+  const uint64_t* start;
+  const uint32_t* deg;
+  const uint32_t* pool;
+  int insert;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+    const uint64_t x = k[i];
+    const uint32_t s = bk.src(x), d = bk.dst(x);
+    const uint32_t* lst = pool + start[s];
+    const uint32_t len = deg[s];
+    const uint32_t pos = lower_bound_u32(lst, len, d);
+    const bool present = pos < len && lst[pos] == d;
+    return insert ? !present : present;
+  }
+};
+struct ApplyOut {
+  ApplyIn in;
+  uint64_t* out;
+  __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
+    if (in(i)) out[pre] = in.k[i];
+  }
+};
+
+// group heads over the applied arcs
+struct HeadIn {
+  const uint64_t* k;
+  BatchKeys bk;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+    return i == 0 || bk.src(k[i - 1]) != bk.src(k[i]);
+  }
+};
+struct HeadOut {
+  const uint64_t* k;
+  BatchKeys bk;
+  uint32_t* gstart;  // first applied arc of group
+  uint32_t* gsrc;
+  __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
+    if (HeadIn{k, bk}(i)) {
+      gstart[pre] = static_cast<uint32_t>(i);
+      gsrc[pre] = bk.src(k[i]);
+    }
+  }
+};
+
+// per group: new degree / capacity, and whether it needs a fresh allocation
+__global__ void group_plan_k(uint32_t ng, uint32_t A, const uint32_t* gstart, const uint32_t* gsrc,
+                             const uint32_t* deg, const uint32_t* cap, int insert, uint32_t* gcnt, uint32_t* gnewdeg,
+                             uint32_t* gnewcap, uint64_t* galloc, int* underflow) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += stride) {
+    const uint32_t c = (gi + 1 < ng ? gstart[gi + 1] : A) - gstart[gi];
+    const uint32_t s = gsrc[gi];
+    const uint32_t d = deg[s];
+    uint32_t nd;
+    if (insert) {
+      nd = d + c;
+    } else {
+      if (c > d) *underflow = 1;  // metadata.hpp:28-31
+      nd = d - c;
+    }
+    gcnt[gi] = c;
+    gnewdeg[gi] = nd;
+    const bool grow = nd > cap[s];
+    gnewcap[gi] = grow ? cap_for(nd) : cap[s];
+    galloc[gi] = grow ? cap_for(nd) : 0;
+  }
+}
+
+// old list sizes of touched vertices (for staging)
+struct OldDegIn {
+  const uint32_t* gsrc;
+  const uint32_t* deg;
+  __device__ __forceinline__ uint64_t operator()(uint64_t gi) const { return deg[gsrc[gi]]; }
+};
+
+// expand flat index -> group via binary search over an exclusive scan
+__device__ __forceinline__ uint32_t find_group(const uint64_t* scan, uint32_t ng, uint64_t e) {
+  uint32_t lo = 0, hi = ng;  // scan[lo] <= e < scan[hi] (scan[ng] = total)
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (scan[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void stage_old_k(uint32_t ng, const uint64_t* oscan, uint64_t total, const uint32_t* gsrc,
+                            const uint64_t* start, const uint32_t* pool, uint32_t* staged) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint32_t gi = find_group(oscan, ng, e);
+    staged[e] = pool[start[gsrc[gi]] + (e - oscan[gi])];
+  }
+}
+
+// old elements -> their slot in the new list
+__global__ void merge_old_k(uint32_t ng, const uint64_t* oscan, uint64_t total, const uint32_t* gsrc,
+                            const uint32_t* gstart, const uint32_t* gcnt, const uint64_t* akeys, BatchKeys bk,
+                            const uint32_t* staged, const uint64_t* newstart, uint32_t* pool, int insert) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+    const uint32_t gi = find_group(oscan, ng, e);
+    const uint32_t j = static_cast<uint32_t>(e - oscan[gi]);
+    const uint32_t x = staged[e];
+    // rank of x among the group's batch destinations
+    const uint64_t* b = akeys + gstart[gi];
+    uint32_t lo = 0, hi = gcnt[gi];
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (bk.dst(b[mid]) < x) lo = mid + 1; else hi = mid;
+    }
+    uint32_t* out = pool + newstart[gsrc[gi]];
+    if (insert) {
+      out[j + lo] = x;
+    } else {
+      const bool removed = lo < gcnt[gi] && bk.dst(b[lo]) == x;
+      if (!removed) out[j - lo] = x;
+    }
+  }
+}
+
+// new elements (insert only) -> their slot
+__global__ void merge_new_k(uint32_t ng, uint32_t A, const uint32_t* gstart, const uint32_t* gsrc,
+                            const uint64_t* akeys, BatchKeys bk, const uint64_t* oscan, const uint32_t* staged,
+                            const uint64_t* newstart, uint32_t* pool) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < A; i += stride) {
+    // group of arc i: last head <= i
+    uint32_t lo = 0, hi = ng;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (gstart[mid] <= i) lo = mid; else hi = mid;
+    }
+    const uint32_t gi = lo;
+    const uint32_t r = static_cast<uint32_t>(i - gstart[gi]);
+    const uint32_t x = bk.dst(akeys[i]);
+    const uint32_t* old = staged + oscan[gi];
+    const uint32_t olen = static_cast<uint32_t>(oscan[gi + 1] - oscan[gi]);
+    pool[newstart[gsrc[gi]] + r + lower_bound_u32(old, olen, x)] = x;
+  }
+}
+
+// destination of each touched list: in place, or a fresh bump allocation
+__global__ void plan_dest_k(uint32_t ng, const uint32_t* gsrc, const uint64_t* galloc_scan, const uint64_t* galloc,
+                            uint64_t pool_top, const uint64_t* start, uint64_t* newstart) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += stride) {
+    const uint32_t s = gsrc[gi];
+    newstart[s] = galloc[gi] ? pool_top + galloc_scan[gi] : start[s];
+  }
+}
+
+__global__ void finish_groups_k(uint32_t ng, const uint32_t* gsrc, const uint32_t* gnewdeg, const uint32_t* gnewcap,
+                                const uint64_t* newstart, uint64_t* start, uint32_t* deg, uint32_t* cap) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += stride) {
+    const uint32_t s = gsrc[gi];
+    start[s] = newstart[s];
+    deg[s] = gnewdeg[gi];
+    cap[s] = gnewcap[gi];
+  }
+}
+
+__global__ void refresh_caps_k(uint64_t n, const uint32_t* deg, uint32_t* cap) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) cap[v] = cap_for(deg[v]);
+}
+
+// prepare(GlobalSort) on the device; returns the unique, self-loop-free
+// keys (sorted) and their count.
+uint64_t prepare_device(gbg_graph* g, const uint32_t* pairs, uint64_t count, BatchKeys bk, uint64_t** ukeys_out) {
+  uint64_t* keys = g->ws.get<uint64_t>("upd.keys", count);
+  uint64_t* sorted = g->ws.get<uint64_t>("upd.sorted", count);
+  int* bad = g->ws.get<int>("upd.bad", 1);
+  GBG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+  GBG_LAUNCH(g, make_keys_k, grid_for(count, 256), 256, 0, pairs, count, g->n, bk, keys, bad);
+  int hb = 0;
+  read_scalars(g, bad, sizeof(hb), &hb);
+  if (hb) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
+  const uint64_t U = sort_unique_keys(g, keys, sorted, count, bk, keys, "upd");
+  *ukeys_out = keys;
+  return U;
+}
+
+uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bool insert) {
+  if (g->kind != GBG_KIND_BLOCKED)
+    fail(GBG_ERR_UNSUPPORTED, insert ? "container is static: batch insert not supported"
+                                     : "container is static: batch delete not supported");
+  if (count == 0) return 0;
+  if (count > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "batch too large (max 2^32-1 arcs)");
+  const BatchKeys bk{key_bits(g->n)};
+  uint64_t* ukeys = nullptr;
+  const uint32_t U = static_cast<uint32_t>(prepare_device(g, pairs_dev, count, bk, &ukeys));
+  if (U == 0) return 0;
+  uint32_t* cnt = g->ws.get<uint32_t>("upd.cnt", 4);
+  uint64_t* akeys = g->ws.get<uint64_t>("upd.sorted", count);  // sorted buffer is free now
+  ApplyIn ain{ukeys, bk, g->bstart, g->bdeg, g->pool, insert ? 1 : 0};
+  device_scan<uint32_t>(g, ain, ApplyOut{ain, akeys}, U, cnt + 1, "upd.apply");
+  uint32_t A = 0;
+  read_scalars(g, cnt + 1, sizeof(A), &A);
+  if (A == 0) return 0;
+  uint32_t* gstart = g->ws.get<uint32_t>("upd.gstart", A + 1);
+  uint32_t* gsrc = g->ws.get<uint32_t>("upd.gsrc", A);
+  device_scan<uint32_t>(g, HeadIn{akeys, bk}, HeadOut{akeys, bk, gstart, gsrc}, A, cnt + 2, "upd.heads");
+  uint32_t ng = 0;
+  read_scalars(g, cnt + 2, sizeof(ng), &ng);
+  uint32_t* gcnt = g->ws.get<uint32_t>("upd.gcnt", ng);
+  uint32_t* gnewdeg = g->ws.get<uint32_t>("upd.gnewdeg", ng);
+  uint32_t* gnewcap = g->ws.get<uint32_t>("upd.gnewcap", ng);
+  uint64_t* galloc = g->ws.get<uint64_t>("upd.galloc", ng);
+  uint64_t* gascan = g->ws.get<uint64_t>("upd.gascan", ng + 1);
+  int* under = g->ws.get<int>("upd.under", 1);
+  for (int attempt = 0;; ++attempt) {
+    GBG_CUDA(cudaMemsetAsync(under, 0, sizeof(int), g->stream));
+    GBG_LAUNCH(g, group_plan_k, grid_for(ng, 256), 256, 0, ng, A, gstart, gsrc, g->bdeg, g->bcap, insert ? 1 : 0,
+               gcnt, gnewdeg, gnewcap, galloc, under);
+    device_scan<uint64_t>(g, ArrayIn<uint64_t>{galloc}, ArrayOut<uint64_t>{gascan}, ng, gascan + ng, "upd.alloc");
+    uint64_t need = 0;
+    read_scalars(g, gascan + ng, sizeof(need), &need);
+    int hu = 0;
+    read_scalars(g, under, sizeof(hu), &hu);
+    if (hu) fail(GBG_ERR_LOGIC, "metadata underflow: tracker and container diverged");
+    if (g->pool_top + need <= g->pool_cap) break;
+    if (attempt > 0) fail(GBG_ERR_OOM, "blocked pool exhausted after compaction");
+    // compact into a larger pool (caps refreshed to the current degrees)
+    GBG_LAUNCH(g, refresh_caps_k, grid_for(g->n, 256), 256, 0, g->n, g->bdeg, g->bcap);
+    blocked_relayout(g, g->bstart, g->pool, 2 * need, true);
+  }
+  // stage the touched old lists
+  uint64_t* oscan = g->ws.get<uint64_t>("upd.oscan", ng + 1);
+  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg}, ArrayOut<uint64_t>{oscan}, ng, oscan + ng, "upd.oscan");
+  uint64_t otot = 0;
+  read_scalars(g, oscan + ng, sizeof(otot), &otot);
+  uint32_t* staged = g->ws.get<uint32_t>("upd.staged", otot);
+  if (otot)
+    GBG_LAUNCH(g, stage_old_k, grid_for(otot, 256, g->sm_count * 16), 256, 0, ng, oscan, otot, gsrc, g->bstart,
+               g->pool, staged);
+  // destinations
+  uint64_t* newstart = g->ws.get<uint64_t>("upd.newstart", g->n);
+  GBG_LAUNCH(g, plan_dest_k, grid_for(ng, 256), 256, 0, ng, gsrc, gascan, galloc, g->pool_top, g->bstart, newstart);
+  if (otot)
+    GBG_LAUNCH(g, merge_old_k, grid_for(otot, 256, g->sm_count * 16), 256, 0, ng, oscan, otot, gsrc, gstart, gcnt,
+               akeys, bk, staged, newstart, g->pool, insert ? 1 : 0);
+  if (insert)
+    GBG_LAUNCH(g, merge_new_k, grid_for(A, 256, g->sm_count * 16), 256, 0, ng, A, gstart, gsrc, akeys, bk, oscan,
+               staged, newstart, g->pool);
+  GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,
+             g->bcap);
+  uint64_t need = 0;
+  read_scalars(g, gascan + ng, sizeof(need), &need);
+  g->pool_top += need;
+  if (insert) {
+    g->m += A;
+  } else {
+    g->m -= A;
+  }
+  g->invalidate_derived();
+  g->symmetric = false;  // arbitrary batches need not keep arc pairs
+  return A;
+}
+
+}  // namespace gbg
+
+using namespace gbg;
+
+extern "C" {
+
+gbg_status gbg_blocked_create(uint64_t n, const uint32_t* arcs, uint64_t m, gbg_graph** out) {
+  return guard([&] {
+    if (!out || (m && !arcs)) fail(GBG_ERR_INVALID_ARGUMENT, "gbg_blocked_create: null argument");
+    *out = nullptr;
+    // validate through the CSR builder (sorted, unique, in range), then lay out
+    gbg_graph* csr = nullptr;
+    gbg_status st = gbg_csr_from_arcs(n, arcs, m, &csr);
+    if (st != GBG_OK) fail(st, gbg_last_error());
+    std::unique_ptr<gbg_graph> hold_csr(csr);
+    gbg_graph* g = new_handle(GBG_KIND_BLOCKED, n);
+    std::unique_ptr<gbg_graph> hold(g);
+    DeviceScope ds(g->device);
+    g->m = m;
+    GBG_CUDA(cudaStreamSynchronize(csr->stream));
+    blocked_from_device_csr(g, n, csr->off, csr->nbr);
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+    *out = hold.release();
+  });
+}
+
+gbg_status gbg_blocked_from_csr(gbg_graph* csr, gbg_graph** out) {
+  return guard([&] {
+    GBG_HANDLE(csr);
+    if (!out) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    if (csr->kind != GBG_KIND_CSR) fail(GBG_ERR_INVALID_ARGUMENT, "gbg_blocked_from_csr: not a CSR handle");
+    *out = nullptr;
+    GBG_CUDA(cudaStreamSynchronize(csr->stream));
+    gbg_graph* g = new_handle(GBG_KIND_BLOCKED, csr->n);
+    std::unique_ptr<gbg_graph> hold(g);
+    g->m = csr->m;
+    blocked_from_device_csr(g, csr->n, csr->off, csr->nbr);
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+    *out = hold.release();
+  });
+}
+
+static gbg_status batch_entry(gbg_graph* g, const uint32_t* arcs, uint64_t count, uint64_t* applied, bool insert,
+                              bool host) {
+  return guard([&] {
+    GBG_HANDLE(g);
+    if (!applied || (count && !arcs)) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    if (g->kind != GBG_KIND_BLOCKED)
+      fail(GBG_ERR_UNSUPPORTED, insert ? "container is static: batch insert not supported"
+                                       : "container is static: batch delete not supported");
+    const uint32_t* dev = arcs;
+    if (host && count) {
+      uint32_t* buf = g->ws.get<uint32_t>("upd.host", 2 * count);
+      GBG_CUDA(cudaMemcpyAsync(buf, arcs, 2 * count * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream));
+      dev = buf;
+    }
+    *applied = apply_batch(g, dev, count, insert);
+  });
+}
+
+gbg_status gbg_insert_batch(gbg_graph* g, const uint32_t* arcs, uint64_t count, uint64_t* applied) {
+  return batch_entry(g, arcs, count, applied, true, true);
+}
+gbg_status gbg_delete_batch(gbg_graph* g, const uint32_t* arcs, uint64_t count, uint64_t* applied) {
+  return batch_entry(g, arcs, count, applied, false, true);
+}
+gbg_status gbg_insert_batch_device(gbg_graph* g, const uint32_t* arcs_dev, uint64_t count, uint64_t* applied) {
+  return batch_entry(g, arcs_dev, count, applied, true, false);
+}
+gbg_status gbg_delete_batch_device(gbg_graph* g, const uint32_t* arcs_dev, uint64_t count, uint64_t* applied) {
+  return batch_entry(g, arcs_dev, count, applied, false, false);
+}
+
+static gbg_status single_arc(gbg_graph* g, uint32_t src, uint32_t dst, int* changed, bool insert) {
+  return guard([&] {
+    if (!g || !changed) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    if (g->kind != GBG_KIND_BLOCKED)
+      fail(GBG_ERR_UNSUPPORTED, insert ? "container is static: insert not supported"
+                                       : "container is static: delete not supported");
+    // set_graph.hpp:144-149 (check_arc)
+    if (src >= g->n || dst >= g->n) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
+    if (src == dst) fail(GBG_ERR_INVALID_ARGUMENT, "self-loops are rejected at ingestion");
+    uint32_t pair[2] = {src, dst};
+    uint64_t applied = 0;
+    gbg_status st = batch_entry(g, pair, 1, &applied, insert, true);
+    if (st != GBG_OK) fail(st, gbg_last_error());
+    *changed = applied ? 1 : 0;
+  });
+}
+
+gbg_status gbg_insert_edge(gbg_graph* g, uint32_t src, uint32_t dst, int* changed) {
+  return single_arc(g, src, dst, changed, true);
+}
+gbg_status gbg_delete_edge(gbg_graph* g, uint32_t src, uint32_t dst, int* changed) {
+  return single_arc(g, src, dst, changed, false);
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Balanced all-edges traversal: the "map_neighbors over every vertex"
+// loop of the reference (e.g. cc, algorithms.cpp:224-227) with the edge
+// list cut into equal tiles instead of per-vertex tasks, so R-MAT hubs
+// (max degree 406,360 at scale 24) spread over many CTAs.  The owning row
+// of each edge comes from a binary search of the degree prefix (`voff`,
+// the CSR offsets or the blocked container's virtual offsets).
+#pragma once
+
+#include "scan.cuh"
+
+namespace gbg {
+
+constexpr int kEdgeThreads = 256;
+constexpr int kEdgeIPT = 8;
+constexpr int kEdgeTile = kEdgeThreads * kEdgeIPT;
+
+__device__ __forceinline__ uint32_t row_of(const uint64_t* voff, uint64_t n, uint64_t e, uint32_t lo) {
+  uint64_t hi = n;  // voff[lo] <= e < voff[hi]
+  uint64_t l = lo;
+  while (hi - l > 1) {
+    uint64_t mid = (l + hi) >> 1;
+    if (voff[mid] <= e) l = mid; else hi = mid;
+  }
+  return static_cast<uint32_t>(l);
+}
+
+// op(u, v, e): arc u -> v, e = its index in voff order
+template <class G, class Op>
+__global__ void __launch_bounds__(kEdgeThreads) for_each_edge_k(G g, const uint64_t* __restrict__ voff, uint64_t m,
+                                                                 Op op) {
+  __shared__ uint32_t s_row[kEdgeTile];
+  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kEdgeTile;
+  if (e0 >= m) return;
+  const uint32_t len = static_cast<uint32_t>(m - e0 < kEdgeTile ? m - e0 : kEdgeTile);
+  {
+    const uint32_t k0 = threadIdx.x * kEdgeIPT;
+    if (k0 < len) {
+      uint32_t r = row_of(voff, g.n, e0 + k0, 0);
+      uint64_t next = voff[r + 1];
+#pragma unroll
+      for (int j = 0; j < kEdgeIPT; ++j) {
+        if (k0 + j >= len) break;
+        if (next <= e0 + k0 + j) {
+          r = row_of(voff, g.n, e0 + k0 + j, r + 1);
+          next = voff[r + 1];
+        }
+        s_row[k0 + j] = r;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < len; k += kEdgeThreads) {
+    const uint32_t u = s_row[k];
+    const uint64_t e = e0 + k;
+    uint32_t v;
+    if (G::kContiguous) {
+      v = g.at(e);
+    } else {
+      v = g.at(g.seg_begin(u) + (e - voff[u]));
+    }
+    op(u, v, e);
+  }
+}
+
+template <class G, class Op>
+void for_each_edge(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Op op) {
+  if (m == 0) return;
+  const uint64_t tiles = (m + kEdgeTile - 1) / kEdgeTile;
+  GBG_LAUNCH(g, (for_each_edge_k<G, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, m, op);
+}
+
+}  // namespace gbg

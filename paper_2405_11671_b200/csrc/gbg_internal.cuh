@@ -1,0 +1,255 @@
+// Internal runtime of libgbg: the device-resident container handle, error
+// plumbing, per-handle workspace, and the two read views every kernel is
+// templated on (CSR and blocked).  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/gbg_c.h"
+
+namespace gbg {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  gbg_status status;
+  Error(gbg_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(gbg_status s, const std::string& m) { throw Error(s, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    fail(GBG_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  fail(GBG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define GBG_CUDA(call) ::gbg::cuda_check((call), #call)
+
+// ---------------------------------------------------------------- memory
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+inline void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// Named, growable device scratch buffers owned by a handle.  Buffers are
+// reused across calls; grow() never shrinks.
+struct Workspace {
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  void* get(const std::string& name, size_t bytes) {
+    Buf& b = bufs[name];
+    if (b.bytes < bytes) {
+      dfree(b.p);
+      b.p = nullptr;
+      b.bytes = 0;
+      size_t want = bytes + bytes / 8 + 256;
+      cuda_check(cudaMalloc(&b.p, want), "workspace cudaMalloc");
+      b.bytes = want;
+    }
+    return b.p;
+  }
+  template <class T>
+  T* get(const std::string& name, size_t count) {
+    return static_cast<T*>(get(name, (count ? count : 1) * sizeof(T)));
+  }
+  void release(const std::string& name) {
+    auto it = bufs.find(name);
+    if (it != bufs.end()) {
+      dfree(it->second.p);
+      bufs.erase(it);
+    }
+  }
+  size_t bytes() const {
+    size_t t = 0;
+    for (auto& kv : bufs) t += kv.second.bytes;
+    return t;
+  }
+  ~Workspace() {
+    for (auto& kv : bufs) dfree(kv.second.p);
+  }
+};
+
+// ---------------------------------------------------------------- views
+// Read view of the static CSR: uint64 offsets[n+1], uint32 neighbors[m],
+// ascending within each segment (csr.hpp:51-52).
+struct CsrView {
+  static constexpr bool kContiguous = true;  // row r's edges start at off[r]
+  uint64_t n;
+  const uint64_t* off;
+  const uint32_t* nbr;
+  __device__ __forceinline__ void seg(uint32_t v, uint64_t& begin, uint32_t& deg) const {
+    uint64_t b = __ldg(off + v), e = __ldg(off + v + 1);
+    begin = b;
+    deg = static_cast<uint32_t>(e - b);
+  }
+  __device__ __forceinline__ uint32_t degree(uint32_t v) const {
+    return static_cast<uint32_t>(__ldg(off + v + 1) - __ldg(off + v));
+  }
+  __device__ __forceinline__ uint32_t at(uint64_t pos) const { return __ldg(nbr + pos); }
+  __device__ __forceinline__ uint64_t seg_begin(uint32_t v) const { return __ldg(off + v); }
+  __device__ __forceinline__ const uint32_t* data() const { return nbr; }
+};
+
+// Read view of the dynamic blocked container: vertex v's ascending
+// neighbours live at pool[start[v] .. start[v]+deg[v]) inside a 16-byte
+// aligned allocation of cap[v] ids (see blocked.cu).
+struct BlockedView {
+  static constexpr bool kContiguous = false;
+  uint64_t n;
+  const uint64_t* start;
+  const uint32_t* deg;
+  const uint32_t* pool;
+  __device__ __forceinline__ void seg(uint32_t v, uint64_t& begin, uint32_t& d) const {
+    begin = __ldg(start + v);
+    d = __ldg(deg + v);
+  }
+  __device__ __forceinline__ uint32_t degree(uint32_t v) const { return __ldg(deg + v); }
+  __device__ __forceinline__ uint32_t at(uint64_t pos) const { return __ldg(pool + pos); }
+  __device__ __forceinline__ uint64_t seg_begin(uint32_t v) const { return __ldg(start + v); }
+  __device__ __forceinline__ const uint32_t* data() const { return pool; }
+};
+
+// ---------------------------------------------------------------- handle
+struct PrSchedule;  // pagerank.cu
+struct TcCache;     // tc.cu
+
+}  // namespace gbg
+
+struct gbg_graph {
+  int kind = GBG_KIND_CSR;
+  int device = 0;
+  uint64_t n = 0;
+  uint64_t m = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  uint64_t launches = 0;
+  int sm_count = 148;
+  bool symmetric = false;  // every arc's reverse present (set by the R-MAT builder)
+
+  // CSR storage
+  uint64_t* off = nullptr;
+  uint32_t* nbr = nullptr;
+
+  // blocked storage (blocked.cu)
+  uint64_t* bstart = nullptr;  // element offset of v's allocation in pool
+  uint32_t* bdeg = nullptr;    // live neighbours
+  uint32_t* bcap = nullptr;    // allocated ids (multiple of 4 -> 16 B)
+  uint32_t* pool = nullptr;
+  uint64_t pool_cap = 0;       // ids
+  uint64_t pool_top = 0;       // ids handed out (bump allocator)
+  uint64_t pool_live = 0;      // ids in live allocations
+
+  // derived, rebuilt lazily after updates
+  uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
+  bool voff_valid = false;
+  gbg::PrSchedule* pr = nullptr;
+
+  gbg::Workspace ws;
+  // pinned host staging for small device->host scalars
+  uint64_t* hscalar = nullptr;
+
+  gbg::CsrView csr_view() const { return {n, off, nbr}; }
+  gbg::BlockedView blocked_view() const { return {n, bstart, bdeg, pool}; }
+  void invalidate_derived();
+  ~gbg_graph();
+};
+
+namespace gbg {
+
+// kernels launched through this macro are counted per handle
+#define GBG_LAUNCH(g, kernel, grid, block, smem, ...)                        \
+  do {                                                                       \
+    kernel<<<(grid), (block), (smem), (g)->stream>>>(__VA_ARGS__);           \
+    ::gbg::cuda_check(cudaGetLastError(), #kernel);                          \
+    (g)->launches++;                                                         \
+  } while (0)
+
+inline unsigned grid_for(uint64_t items, unsigned per_block, unsigned cap = 148u * 64u) {
+  uint64_t g = (items + per_block - 1) / per_block;
+  if (g == 0) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+// Read small device scalars back (synchronises the handle's stream).
+void read_scalars(gbg_graph* g, const void* dev, size_t bytes, void* host);
+
+// Dispatch a functor templated on the view type.
+template <class F>
+void with_view(gbg_graph* g, F&& f) {
+  if (g->kind == GBG_KIND_CSR)
+    f(g->csr_view());
+  else
+    f(g->blocked_view());
+}
+
+// Ensure the blocked container's virtual offsets (scan of degrees) are
+// current; returns a pointer usable as CSR-like offsets for scheduling.
+const uint64_t* virtual_offsets(gbg_graph* g);
+
+}  // namespace gbg
+
+namespace gbg {
+
+void set_last_error(const std::string& m);
+
+// Run `f`, translating exceptions into a status + thread-local message.
+template <class F>
+gbg_status guard(F&& f) {
+  try {
+    f();
+    return GBG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::bad_alloc& e) {
+    set_last_error(e.what());
+    return GBG_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return GBG_ERR_LOGIC;
+  }
+}
+
+// Make the handle's device current for the duration of a call.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Locked, device-scoped access to a handle.
+#define GBG_HANDLE(g)                                                        \
+  if (!(g)) ::gbg::fail(GBG_ERR_INVALID_ARGUMENT, "null graph handle");     \
+  std::lock_guard<std::mutex> gbg_lock_((g)->mu);                            \
+  ::gbg::DeviceScope gbg_dev_((g)->device)
+
+gbg_graph* new_handle(int kind, uint64_t n);
+void build_csr_offsets_from_sorted_src(gbg_graph* g, const uint32_t* src, uint64_t m, uint64_t* off);
+void blocked_from_device_csr(gbg_graph* g, uint64_t n, const uint64_t* off, const uint32_t* nbr);
+
+}  // namespace gbg

@@ -1,0 +1,151 @@
+// Device-wide exclusive scan / compaction building block (reduce-then-scan,
+// three launches).  Input and output are functors so the same code serves
+// degree prefix sums (frontier work, CSR offsets, tile schedules) and
+// stream compaction (scatter inside the output functor).
+#pragma once
+
+#include "gbg_internal.cuh"
+
+namespace gbg {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr uint64_t kScanTile = kScanThreads * kScanItems;
+
+template <class T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// Exclusive scan across the block; every thread gets its exclusive prefix
+// and the block total.  smem: >= 33 T.  Contains __syncthreads.
+template <class T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane == 31) smem[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < nwarps ? smem[lane] : T(0);
+    T wi = warp_inclusive_scan(w);
+    if (lane < nwarps) smem[lane] = wi - w;
+    if (lane == nwarps - 1) smem[32] = wi;
+  }
+  __syncthreads();
+  T res = smem[warp] + inc - v;
+  total = smem[32];
+  __syncthreads();
+  return res;
+}
+
+// Deterministic block sum (fixed tree).  smem >= 33 T.
+template <class T>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < nwarps ? smem[lane] : T(0);
+    w = warp_sum(w);
+    if (lane == 0) smem[32] = w;
+  }
+  __syncthreads();
+  T r = smem[32];
+  __syncthreads();
+  return r;
+}
+
+template <class T, class In>
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_k(In in, uint64_t count, T* sums) {
+  __shared__ T sm[33];
+  uint64_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  T acc = 0;
+#pragma unroll 4
+  for (int j = 0; j < kScanItems; ++j)
+    if (base + j < count) acc += in(base + j);
+  T t = block_sum<T>(acc, sm);
+  if (threadIdx.x == 0) sums[blockIdx.x] = t;
+}
+
+template <class T>
+__global__ void __launch_bounds__(1024) scan_sums_k(T* sums, uint64_t nb, T* total) {
+  __shared__ T sm[33];
+  uint64_t per = (nb + blockDim.x - 1) / blockDim.x;
+  uint64_t b = threadIdx.x * per, e = b + per < nb ? b + per : nb;
+  T acc = 0;
+  for (uint64_t i = b; i < e; ++i) acc += sums[i];
+  T tot;
+  T pre = block_exclusive_scan<T>(acc, sm, tot);
+  for (uint64_t i = b; i < e; ++i) {
+    T s = sums[i];
+    sums[i] = pre;
+    pre += s;
+  }
+  if (threadIdx.x == 0 && total) *total = tot;
+}
+
+template <class T, class In, class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_down_k(In in, Out out, uint64_t count, const T* sums) {
+  __shared__ T sm[33];
+  uint64_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  T vals[kScanItems];
+  T acc = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    vals[j] = base + j < count ? in(base + j) : T(0);
+    acc += vals[j];
+  }
+  T tot;
+  T pre = block_exclusive_scan<T>(acc, sm, tot) + sums[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (base + j < count) out(base + j, pre);
+    pre += vals[j];
+  }
+}
+
+// Exclusive scan of in(0..count) delivered to out(i, prefix); the grand total
+// lands in *total_dev (device pointer, may be null).  No host sync.
+template <class T, class In, class Out>
+void device_scan(gbg_graph* g, In in, Out out, uint64_t count, T* total_dev, const char* tag = "scan") {
+  uint64_t nb = (count + kScanTile - 1) / kScanTile;
+  if (nb == 0) nb = 1;
+  T* sums = g->ws.get<T>(std::string(tag) + ".sums", nb);
+  GBG_LAUNCH(g, (scan_reduce_k<T, In>), (unsigned)nb, kScanThreads, 0, in, count, sums);
+  GBG_LAUNCH(g, scan_sums_k<T>, 1, 1024, 0, sums, nb, total_dev);
+  GBG_LAUNCH(g, (scan_down_k<T, In, Out>), (unsigned)nb, kScanThreads, 0, in, out, count, sums);
+}
+
+// Common functors
+struct NullOut {
+  template <class T>
+  __device__ __forceinline__ void operator()(uint64_t, T) const {}
+};
+template <class T>
+struct ArrayIn {
+  const T* a;
+  __device__ __forceinline__ T operator()(uint64_t i) const { return a[i]; }
+};
+template <class T>
+struct ArrayOut {
+  T* a;
+  __device__ __forceinline__ void operator()(uint64_t i, T v) const { a[i] = v; }
+};
+
+}  // namespace gbg

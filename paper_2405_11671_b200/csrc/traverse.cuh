@@ -1,0 +1,214 @@
+// vertex_subset conversions and the two edge_map engines as device
+// templates over a read view (CsrView / BlockedView) and an operator:
+//
+//   struct Op {
+//     __device__ bool cond(uint32_t v);            // EdgeMapSpec::cond
+//     __device__ bool claim(uint32_t v);           // push dedup (AtomicBitset::try_claim)
+//     __device__ bool update(uint32_t u, uint32_t v);  // EdgeMapSpec::update
+//     __device__ void dense_word(uint64_t w, uint32_t emitted_mask);  // pull: word owner hook
+//   };
+//
+// Reference semantics: traversal.cpp:16-46 (sparse push: cond, claim, then
+// update; at most one update per destination), traversal.cpp:48-95 (dense
+// pull over every v with cond(v), scanning N(v) against the frontier
+// bitmap, early exit at the first frontier neighbour whose update returns
+// true), traversal.cpp:101-111 (switch).  Ops used with early exit must
+// return true from update (BFS and the test op do).
+//
+// Bitmaps are uint32 words, bit v&31 of word v>>5 — byte-identical on
+// little-endian to the reference's uint64 LSB-first words
+// (vertex_subset.hpp:10-14).
+#pragma once
+
+#include "scan.cuh"
+
+namespace gbg {
+
+__device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t v) {
+  return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------- subsets
+__global__ void list_to_bitmap_k(const uint32_t* ids, uint64_t k, uint32_t* bm);
+
+struct PopcIn {
+  const uint32_t* bm;
+  __device__ __forceinline__ uint32_t operator()(uint64_t w) const { return __popc(bm[w]); }
+};
+struct BitsToIdsOut {
+  const uint32_t* bm;
+  uint32_t* ids;
+  __device__ __forceinline__ void operator()(uint64_t w, uint32_t pre) const {
+    uint32_t bits = bm[w];
+    while (bits) {
+      int b = __ffs(bits) - 1;
+      ids[pre++] = static_cast<uint32_t>(w * 32 + b);
+      bits &= bits - 1;
+    }
+  }
+};
+
+// ascending compaction of a bitmap into an id list; *count_dev = size
+inline void bitmap_to_list(gbg_graph* g, const uint32_t* bm, uint64_t nwords, uint32_t* ids, uint32_t* count_dev) {
+  device_scan<uint32_t>(g, PopcIn{bm}, BitsToIdsOut{bm, ids}, nwords, count_dev, "b2l");
+}
+
+// ---------------------------------------------------------------- push
+constexpr int kPushThreads = 256;
+constexpr int kPushIPT = 8;
+constexpr int kPushTile = kPushThreads * kPushIPT;
+
+template <class G>
+struct FrontierDegIn {
+  G g;
+  const uint32_t* F;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return g.degree(F[i]); }
+};
+
+// Load-balanced expansion over the frontier's edges: tile t owns edges
+// [t*kPushTile, (t+1)*kPushTile) of the concatenated neighbour lists; the
+// owning frontier slot of each edge comes from a per-thread binary search
+// of the exclusive degree scan, then edges are walked with consecutive
+// threads on consecutive neighbours (coalesced within a list).
+template <class G, class Op>
+__global__ void __launch_bounds__(kPushThreads)
+    push_k(G g, const uint32_t* __restrict__ F, uint32_t nf, const uint64_t* __restrict__ dscan,
+           uint64_t E, Op op, uint32_t* __restrict__ out, unsigned long long* counters) {
+  __shared__ uint32_t s_idx[kPushTile];
+  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kPushTile;
+  if (e0 >= E) return;
+  const uint32_t len = static_cast<uint32_t>(E - e0 < kPushTile ? E - e0 : kPushTile);
+  {
+    const uint32_t k0 = threadIdx.x * kPushIPT;
+    if (k0 < len) {
+      const uint64_t e = e0 + k0;
+      uint32_t lo = 0, hi = nf;  // dscan[lo] <= e < dscan[hi]
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (dscan[mid] <= e) lo = mid; else hi = mid;
+      }
+      uint32_t i = lo;
+      uint64_t next = dscan[i + 1];
+#pragma unroll
+      for (int j = 0; j < kPushIPT; ++j) {
+        if (k0 + j >= len) break;
+        while (next <= e + j) next = dscan[++i + 1];
+        s_idx[k0 + j] = i;
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  unsigned long long emitted = 0, degsum = 0;
+  for (uint32_t base = 0; base < len; base += kPushThreads) {
+    const uint32_t k = base + threadIdx.x;
+    bool emit = false;
+    uint32_t v = 0;
+    if (k < len) {
+      const uint32_t i = s_idx[k];
+      const uint32_t u = __ldg(F + i);
+      uint64_t b;
+      uint32_t d;
+      g.seg(u, b, d);
+      v = g.at(b + (e0 + k - __ldg(dscan + i)));
+      emit = op.cond(v) && op.claim(v) && op.update(u, v);
+    }
+    const uint32_t mask = __ballot_sync(0xffffffffu, emit);
+    if (mask) {
+      uint32_t pos = 0;
+      const int leader = __ffs(mask) - 1;
+      if (lane == leader) pos = static_cast<uint32_t>(atomicAdd(counters, (unsigned long long)__popc(mask)));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (emit) {
+        out[pos + __popc(mask & ((1u << lane) - 1))] = v;
+        degsum += g.degree(v);
+      }
+      emitted += __popc(mask);
+    }
+  }
+  degsum = warp_sum(degsum);
+  if (lane == 0 && degsum) atomicAdd(counters + 1, degsum);
+}
+
+// ---------------------------------------------------------------- pull
+constexpr int kPullThreads = 256;
+constexpr uint32_t kPullSerial = 8;  // neighbours a lane scans before the warp helps
+
+// One warp per 32-vertex bitmap word (so output / visited words need no
+// atomics).  Each lane first scans up to kPullSerial neighbours of its own
+// vertex; vertices still unresolved with longer lists are then scanned by
+// the whole warp, 32 neighbours per step, ballot on frontier hits, stopping
+// at the first hit in list order when early exit applies.
+template <class G, class Op, bool kEarly>
+__global__ void __launch_bounds__(kPullThreads)
+    pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
+           unsigned long long* counters) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long cnt = 0, degsum = 0;
+  for (uint64_t w = warp0; w < nwords; w += nwarps) {
+    const uint64_t v64 = w * 32 + lane;
+    const uint32_t v = static_cast<uint32_t>(v64);
+    const bool c = v64 < g.n && op.cond(v);
+    uint64_t b = 0;
+    uint32_t d = 0;
+    bool found = false;
+    if (c) {
+      g.seg(v, b, d);
+      const uint32_t lim = d < kPullSerial ? d : kPullSerial;
+      for (uint32_t j = 0; j < lim; ++j) {
+        const uint32_t u = g.at(b + j);
+        if (bit_test(fb, u) && op.update(u, v)) {
+          found = true;
+          if (kEarly) break;
+        }
+      }
+    }
+    uint32_t hard = __ballot_sync(0xffffffffu, c && d > kPullSerial && !(kEarly && found));
+    while (hard) {
+      const int l = __ffs(hard) - 1;
+      hard &= hard - 1;
+      const uint64_t bb = __shfl_sync(0xffffffffu, b, l);
+      const uint32_t dd = __shfl_sync(0xffffffffu, d, l);
+      const uint32_t vv = static_cast<uint32_t>(w * 32 + l);
+      bool fl = false;
+      for (uint32_t j0 = kPullSerial; j0 < dd; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        uint32_t u = 0;
+        const bool hit = j < dd && bit_test(fb, u = g.at(bb + j));
+        const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+        if (!hm) continue;
+        if (kEarly) {
+          const int f = __ffs(hm) - 1;
+          bool r = false;
+          if (lane == f) r = op.update(u, vv);
+          if (__shfl_sync(0xffffffffu, r, f)) {
+            fl = true;
+            break;
+          }
+        } else {
+          bool r = hit && op.update(u, vv);
+          if (__ballot_sync(0xffffffffu, r)) fl = true;
+        }
+      }
+      if (lane == l && fl) found = true;
+    }
+    const uint32_t fm = __ballot_sync(0xffffffffu, found);
+    if (fm) {
+      if (lane == 0) {
+        nb[w] = fm;
+        op.dense_word(w, fm);
+      }
+      cnt += __popc(fm);
+      if (found) degsum += d;
+    }
+  }
+  degsum = warp_sum(degsum);
+  if (lane == 0 && cnt) {
+    atomicAdd(counters, cnt);
+    atomicAdd(counters + 1, degsum);
+  }
+}
+
+}  // namespace gbg

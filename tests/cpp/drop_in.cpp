@@ -1,0 +1,210 @@
+// Drop-in test: the device containers behind the reference's own harness.
+//
+// Links the UNMODIFIED reference library (built in place by oracle/Makefile)
+// and libgbg.so through include/gbg/gb_container.hpp, then replays the
+// reference's container-contract assertions with the GPU containers
+// injected where the reference injects extra containers:
+//   - verify_graph with VerifyOptions::extra_containers (bench.cpp:288-347;
+//     acceptance.cpp:134-153: T4 + 10 seeded ER(100, 0.05))
+//   - apply_insert / apply_delete counts on T4 (test_batch.cpp:85-125)
+//   - the RMAT round trip with duplicates (acceptance.cpp:272-320)
+//   - static containers reject updates, CsrGraph::build errors
+//     (test_containers.cpp:26-52)
+//   - all containers agree on degrees and neighbour lists (test_containers.cpp:147-165)
+//   - device bfs / cc / pagerank against gb::bfs / gb::cc / gb::pagerank
+// Prints one PASS/FAIL line per check; exit status = number of failures.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <sstream>
+#include <string>
+
+#include "gb/algorithms.hpp"
+#include "gb/batch.hpp"
+#include "gb/bench.hpp"
+#include "gb/csr.hpp"
+#include "gb/derive.hpp"
+#include "gb/generators.hpp"
+#include "gbg/gb_container.hpp"
+
+using namespace gb;
+
+static int failures = 0;
+
+static void check(const char* name, const std::function<bool(std::string&)>& fn) {
+  std::string detail;
+  bool ok = false;
+  try {
+    ok = fn(detail);
+  } catch (const std::exception& e) {
+    detail = std::string("exception: ") + e.what();
+  }
+  std::printf("%s %s%s%s\n", ok ? "PASS" : "FAIL", name, detail.empty() ? "" : " -- ", detail.c_str());
+  if (!ok) ++failures;
+}
+
+static std::vector<Edge> arc_list(const GraphContainer& c) {
+  GraphView view(c);
+  std::vector<Edge> arcs;
+  for (uint64_t v = 0; v < view.num_vertices(); ++v)
+    for (VertexId u : derive_get_neighbors(view, static_cast<VertexId>(v))) arcs.push_back({static_cast<VertexId>(v), u});
+  return arcs;
+}
+
+int main() {
+  const auto& extra = gbg::gpu_containers();
+
+  check("verify_graph with GPU containers injected (t4 + 10 ER)", [&](std::string& d) {
+    std::ostringstream report;
+    VerifyOptions opts;
+    opts.extra_containers = &extra;
+    GraphData t4 = tiny_fixture_graph();
+    if (!verify_graph(t4, opts, report)) {
+      d = report.str();
+      return false;
+    }
+    for (uint64_t seed = 1; seed <= 10; ++seed) {
+      GraphData g = generate_er({100, 0.05}, seed);
+      g.name = "er100-" + std::to_string(seed);
+      opts.seed = seed;
+      if (!verify_graph(g, opts, report)) {
+        std::istringstream lines(report.str());
+        std::string line;
+        while (std::getline(lines, line))
+          if (line.find("MISMATCH") != std::string::npos) d = line;
+        return false;
+      }
+    }
+    return true;
+  });
+
+  check("apply_insert/apply_delete counts on T4 (gpu_blocked)", [&](std::string& d) {
+    GraphData t4 = tiny_fixture_graph();
+    GraphContainerPtr g = extra[1].build(t4);
+    EdgeBatch add{{{0, 3}, {3, 0}}};
+    PreparedBatch pb = prepare(add, g->preferred_batch_form());
+    if (apply_insert(*g, pb) != 2 || g->num_edges() != 10 || g->degree(3) != 2) return d = "insert", false;
+    PreparedBatch own = prepare(EdgeBatch{t4.arcs}, g->preferred_batch_form());
+    if (apply_insert(*g, own) != 0 || g->num_edges() != 10) return d = "own", false;
+    if (apply_delete(*g, pb) != 2 || g->num_edges() != 8 || arc_list(*g) != t4.arcs) return d = "delete", false;
+    EdgeBatch absent{{{1, 3}, {3, 1}}};
+    if (apply_delete(*g, prepare(absent, g->preferred_batch_form())) != 0) return d = "absent", false;
+    EdgeBatch drop{{{2, 3}, {3, 2}}};
+    if (apply_delete(*g, prepare(drop, g->preferred_batch_form())) != 2 || g->num_edges() != 6)
+      return d = "drop", false;
+    apply_delete(*g, prepare(EdgeBatch{t4.arcs}, g->preferred_batch_form()));
+    return g->num_vertices() == 4 && g->num_edges() == 0;
+  });
+
+  check("single-arc updates (gpu_blocked)", [&](std::string& d) {
+    GraphData t4 = tiny_fixture_graph();
+    GraphContainerPtr g = extra[1].build(t4);
+    if (!g->delete_edge({0, 1}) || g->delete_edge({0, 1}) || !g->insert_edge({0, 1}) || g->insert_edge({0, 1}))
+      return d = "changed flags", false;
+    bool threw = false;
+    try {
+      g->insert_edge({2, 2});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    if (!threw) return d = "self loop accepted", false;
+    threw = false;
+    try {
+      g->insert_edge({0, 9});
+    } catch (const std::out_of_range&) {
+      threw = true;
+    }
+    return threw && arc_list(*g) == t4.arcs;
+  });
+
+  check("batch round trip with duplicates restores the base (acceptance criterion 5)", [&](std::string& d) {
+    RmatParams params;
+    params.log2_n = 14;
+    GraphData base = generate_rmat(params, uint64_t{1} << 16, 11);
+    EdgeBatch raw = generate_update_batch(params, 20000, 777);
+    EdgeBatch batch;
+    for (Edge e : raw.updates)
+      if (!std::binary_search(base.arcs.begin(), base.arcs.end(), e)) batch.updates.push_back(e);
+    size_t half = batch.updates.size() / 2;
+    batch.updates.insert(batch.updates.end(), batch.updates.begin(), batch.updates.begin() + half);
+    GraphContainerPtr ref = container_by_name("chunked_set").build(base);
+    GraphContainerPtr g = extra[1].build(base);
+    uint64_t ri = apply_insert(*ref, prepare(batch, BatchForm::GlobalSort));
+    uint64_t gi = apply_insert(*g, prepare(batch, g->preferred_batch_form()));
+    if (ri != gi || gi == 0) return d = "inserted " + std::to_string(gi) + " vs " + std::to_string(ri), false;
+    if (arc_list(*g) != arc_list(*ref)) return d = "arc sets differ after insert", false;
+    uint64_t gd = apply_delete(*g, prepare(batch, g->preferred_batch_form()));
+    if (gd != gi) return d = "deleted != inserted", false;
+    return g->num_edges() == base.arcs.size() && arc_list(*g) == base.arcs;
+  });
+
+  check("static device CSR rejects updates; build validates input", [&](std::string& d) {
+    GraphData t4 = tiny_fixture_graph();
+    GraphContainerPtr g = extra[0].build(t4);
+    int thrown = 0;
+    try { g->insert_edge({0, 3}); } catch (const unsupported_operation&) { ++thrown; }
+    try { g->delete_edge({0, 1}); } catch (const unsupported_operation&) { ++thrown; }
+    try { g->insert_sorted_batch({}); } catch (const unsupported_operation&) { ++thrown; }
+    try { g->delete_sorted_batch({}); } catch (const unsupported_operation&) { ++thrown; }
+    if (thrown != 4) return d = "updates accepted", false;
+    std::vector<Edge> unsorted = {{1, 0}, {0, 1}}, dup = {{0, 1}, {0, 1}}, oor = {{0, 5}};
+    int fmt = 0;
+    for (auto* a : {&unsorted, &dup, &oor}) {
+      try { gbg::GpuCsrGraph::build(2, *a); } catch (const format_error&) { ++fmt; }
+    }
+    return fmt == 3;
+  });
+
+  check("containers agree on degrees and neighbours (random graph)", [&](std::string& d) {
+    GraphData g = generate_er({100, 0.05}, 23);
+    CsrGraph reference = CsrGraph::build(g.n, g.arcs);
+    GraphView rv(reference);
+    for (const auto& info : extra) {
+      GraphContainerPtr c = info.build(g);
+      GraphView view(*c);
+      if (view.num_vertices() != g.n || view.num_edges() != g.arcs.size()) return d = info.name, false;
+      for (uint64_t v = 0; v < g.n; ++v) {
+        if (view.degree(v) != rv.degree(v)) return d = info.name + " degree", false;
+        if (derive_get_neighbors(view, v) != derive_get_neighbors(rv, v)) return d = info.name + " nbrs", false;
+      }
+      if (c->memory_bytes() == 0) return d = "memory_bytes", false;
+    }
+    return true;
+  });
+
+  check("device bfs / cc / pagerank match gb:: on seeded graphs", [&](std::string& d) {
+    for (int trial = 0; trial < 20; ++trial) {
+      GraphData g = generate_er({150, 0.03}, 100 + trial);
+      CsrGraph cpu = CsrGraph::build(g.n, g.arcs);
+      GraphView cv(cpu);
+      for (const auto& info : extra) {
+        GraphContainerPtr c = info.build(g);
+        const auto& dev = dynamic_cast<const gbg::GpuGraph&>(*c);
+        if (gbg::bfs_distances(dev, trial % 150) != bfs(cv, trial % 150).distances) return d = "bfs", false;
+        if (gbg::cc(dev) != cc(cv)) return d = "cc", false;
+        auto a = gbg::pagerank(dev, 0.85, 20, 1e-4);
+        auto b = pagerank(cv, 0.85, 20, 1e-4);
+        double l1 = 0;
+        for (size_t v = 0; v < a.size(); ++v) l1 += std::abs(a[v] - b[v]);
+        if (!(l1 < 1e-12)) return d = "pagerank l1 " + std::to_string(l1), false;
+      }
+    }
+    // the AlgorithmInfo entries on an unmasked view
+    GraphData t4 = tiny_fixture_graph();
+    GraphContainerPtr c = extra[0].build(t4);
+    GraphView v(*c);
+    AlgoParams p;
+    for (const auto& a : gbg::gpu_algorithms()) {
+      CanonicalOutput dev = a.run(v, p);
+      CsrGraph cpu = CsrGraph::build(t4.n, t4.arcs);
+      GraphView cv(cpu);
+      CanonicalOutput want = algorithm_by_name(a.name).run(cv, p);
+      if (a.name != "pagerank" && dev.digest() != want.digest()) return d = a.name, false;
+    }
+    return true;
+  });
+
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}

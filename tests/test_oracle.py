@@ -1,0 +1,311 @@
+"""CPU tests: pin the C restatement oracle (oracle/gbo.c) against the
+reference library itself (oracle/_ref/libgbref.so, built from
+/root/reference) and against the reference test suite's known answers and
+the golden fixtures.  No GPU needed."""
+import numpy as np
+import pytest
+
+from oracle.bindings import digest, max_degree_source
+from tests.conftest import golden
+from tests.helpers import T4_PAIRS, complete, csr, members, star, undirected
+
+TINY = np.finfo(np.float64).tiny
+
+
+# ---------------------------------------------------------------- generators
+@pytest.mark.parametrize("a,b,c", [(0.5, 0.1, 0.1), (0.57, 0.19, 0.19)])
+@pytest.mark.parametrize("seed", [1, 42, 12345])
+def test_update_batch_matches_reference(ref, orc, a, b, c, seed):
+    for log2_n in (4, 14, 22):
+        x = ref.update_batch(log2_n, 1000, seed, a, b, c)
+        y = orc.update_batch(log2_n, 1000, seed, a, b, c)
+        assert np.array_equal(x, y)
+
+
+def test_update_batch_shape_and_pairs(orc):
+    # test_batch.cpp:162-182
+    one = orc.update_batch(14, 10, 42, 0.5, 0.1, 0.1)
+    assert one.shape == (20, 2)
+    assert np.array_equal(one[0::2, 0], one[1::2, 1]) and np.array_equal(one[0::2, 1], one[1::2, 0])
+    assert np.array_equal(one, orc.update_batch(14, 10, 42, 0.5, 0.1, 0.1))
+    assert not np.array_equal(one, orc.update_batch(14, 10, 43, 0.5, 0.1, 0.1))
+
+
+def test_rng_and_hash_match_reference(ref, orc):
+    for a, b in [(0, 0), (1, 2), (2**63, 7), (123456789, 987654321)]:
+        assert ref.L.gbref_hash_combine(a, b) == orc.L.gbo_hash_combine(a, b)
+    for s, st, cn in [(1, 0, 0), (1, 5, 3), (99, 2**40, 17)]:
+        assert ref.L.gbref_rng_double(s, st, cn) == orc.L.gbo_rng_double(s, st, cn)
+
+
+@pytest.mark.parametrize("S", [10, 14])
+def test_rmat_graph_matches_reference(ref, orc, S):
+    n1, p1 = ref.rmat(S, 16 << S, 1)
+    n2, p2 = orc.rmat(S, 16 << S, 1)
+    assert n1 == n2 == 1 << S
+    assert np.array_equal(p1, p2)
+
+
+def test_rmat_s16_matches_golden(orc):
+    gd = golden(16)
+    n, pairs = orc.rmat(16, 16 << 16, 1)
+    off, nbr = csr(n, pairs)
+    assert (n, int(off[n])) == (gd["n"], gd["m"])
+    assert digest(off) == gd["off_digest"] and digest(nbr) == gd["nbr_digest"]
+
+
+def test_normalize_and_fixture(ref, orc):
+    n, p = ref.t4()
+    assert n == 4 and np.array_equal(p, T4_PAIRS)
+    n2, p2 = orc.normalize([[0, 1], [1, 2], [0, 2], [2, 3]], 4)
+    assert n2 == 4 and np.array_equal(p2, T4_PAIRS)
+    # n = max(min_n, 1 + max id), loops counted for n but dropped
+    n3, p3 = orc.normalize([[5, 5], [0, 1]], 0)
+    assert n3 == 6 and p3.tolist() == [[0, 1], [1, 0]]
+
+
+def test_csr_build_known_answers(orc):
+    # test_containers.cpp:17-39
+    off, nbr = orc.csr(4, T4_PAIRS)
+    assert off.tolist() == [0, 2, 4, 7, 8] and nbr.tolist() == [1, 2, 0, 2, 0, 1, 3, 2]
+    off, nbr = orc.csr(3, np.zeros((0, 2), np.uint32))
+    assert off.tolist() == [0, 0, 0, 0]
+    for bad, n in (([[1, 0], [0, 1]], 2), ([[0, 1], [0, 1]], 2), ([[0, 5]], 2)):
+        with pytest.raises(ValueError):
+            orc.csr(n, bad)
+
+
+# ---------------------------------------------------------------- subsets
+def test_subset_known_answers(orc):
+    # test_vertex_subset.cpp:22-57
+    assert orc.to_dense(4, [1, 3]).tolist() == [0b1010]
+    assert orc.to_dense(1000, [999]).size == (1000 + 63) // 64
+    assert orc.to_sparse(4, np.array([0b0101], np.uint64)).tolist() == [0, 2]
+    assert orc.to_sparse(6, orc.to_dense(6, [5, 1, 5, 3, 1])).tolist() == [1, 3, 5]
+    assert orc.to_sparse(4, np.array([0b1111], np.uint64)).tolist() == [0, 1, 2, 3]
+
+
+def test_subset_round_trips(orc):
+    # test_vertex_subset.cpp:69-92
+    rng = np.random.default_rng(42)
+    for _ in range(300):
+        n = int(rng.integers(1, 301))
+        ids = rng.integers(0, n, size=int(rng.integers(0, n + 1))).astype(np.uint32)
+        dense = orc.to_dense(n, ids)
+        back = orc.to_sparse(n, dense)
+        assert back.tolist() == sorted(set(ids.tolist()))
+        assert np.array_equal(orc.to_dense(n, back), dense)
+
+
+# ---------------------------------------------------------------- edge_map
+def test_edge_map_known_answers(ref, orc):
+    off, nbr = csr(4, T4_PAIRS)
+    g = ref.csr(4, off, nbr)
+    allc = np.ones(4, np.uint8)
+    # T4 bfs step {0} -> {1,2} (test_traversal.cpp:25-44)
+    cond = np.array([0, 1, 1, 1], np.uint8)
+    for mode in (0, 1):
+        out, upd = orc.edge_map(4, off, nbr, [0], cond, mode)
+        assert members(out) == {1, 2}
+        rout, rupd, _ = g.edge_map([0], cond, mode)
+        assert members(rout) == {1, 2} and rupd == upd
+    # empty frontier, always-false cond (46-61)
+    assert members(orc.edge_map(4, off, nbr, [], allc, 0)[0]) == set()
+    assert members(orc.edge_map(4, off, nbr, [0, 1, 2, 3], np.zeros(4, np.uint8), 1)[0]) == set()
+    # pull step with cond v == 3 (63-75)
+    assert members(orc.edge_map(4, off, nbr, [1, 2], np.array([0, 0, 0, 1], np.uint8), 1)[0]) == {3}
+
+
+def test_dense_early_exit_counts(ref, orc):
+    # test_traversal.cpp:77-114: star 0-(1..63), frontier 1..63, cond v == 0
+    n, pairs = undirected(64, star(63), orc)
+    off, nbr = csr(n, pairs)
+    cond = np.zeros(64, np.uint8)
+    cond[0] = 1
+    ids = np.arange(1, 64, dtype=np.uint32)
+    assert orc.edge_map(n, off, nbr, ids, cond, 1, True)[1] == 1
+    assert orc.edge_map(n, off, nbr, ids, cond, 1, False)[1] == 63
+    g = ref.csr(n, off, nbr)
+    assert g.edge_map(ids, cond, 1, True)[1] == 1
+    assert g.edge_map(ids, cond, 1, False)[1] == 63
+
+
+def test_sparse_once_per_destination(orc):
+    # test_traversal.cpp:138-161
+    n, pairs = undirected(32, star(31), orc)
+    off, nbr = csr(n, pairs)
+    out, upd = orc.edge_map(n, off, nbr, np.arange(1, 32), np.ones(32, np.uint8), 0)
+    assert upd == 1 and members(out) == {0}
+
+
+def test_modes_agree_on_seeded_graphs(ref, orc):
+    # test_traversal.cpp:163-185 / acceptance.cpp:238-268 (same construction)
+    rng = np.random.default_rng(7)
+    for trial in range(60):
+        nv = 40 + int(rng.integers(0, 40))
+        n, pairs = ref.er(nv, 0.08, 1000 + trial)
+        off, nbr = csr(n, pairs)
+        ids = np.nonzero(rng.integers(0, 3, size=n) == 0)[0].astype(np.uint32)
+        cond = (rng.integers(0, 4, size=n) != 0).astype(np.uint8)
+        a, _ = orc.edge_map(n, off, nbr, ids, cond, 0)
+        b, _ = orc.edge_map(n, off, nbr, ids, cond, 1)
+        assert members(a) == members(b)
+        r, _, _ = ref.csr(n, off, nbr).edge_map(ids, cond, 0)
+        assert members(r) == members(a)
+
+
+def test_two_hubs(orc):
+    # test_traversal.cpp:220-237
+    edges = [(0, v) for v in range(2, 1502)] + [(1, v) for v in range(1502, 3002)]
+    n, pairs = undirected(3002, edges, orc)
+    off, nbr = csr(n, pairs)
+    cond = np.ones(n, np.uint8)
+    cond[:2] = 0
+    out, _ = orc.edge_map(n, off, nbr, [0, 1], cond, 0)
+    m = sorted(members(out))
+    assert len(m) == 3000 and m[0] == 2 and m[-1] == 3001
+
+
+# ---------------------------------------------------------------- algorithms
+def test_bfs_known_answers(orc):
+    off, nbr = csr(4, T4_PAIRS)
+    assert orc.bfs(4, off, nbr, 0)[0].tolist() == [0, 1, 1, 2]
+    n, pairs = undirected(4, [(0, 1)], orc)
+    off, nbr = csr(n, pairs)
+    assert orc.bfs(n, off, nbr, 3)[0].tolist() == [-1, -1, -1, 0]
+    with pytest.raises(IndexError):
+        orc.bfs(4, *csr(4, T4_PAIRS), 9)
+
+
+def test_bfs_matches_reference_on_seeded_graphs(ref, orc):
+    for trial in range(20):
+        n, pairs = ref.er(150, 0.03, 100 + trial)
+        off, nbr = csr(n, pairs)
+        g = ref.csr(n, off, nbr)
+        d, modes, sizes = orc.bfs(n, off, nbr, trial % 150)
+        assert np.array_equal(d, g.bfs(trial % 150))
+        assert (modes, sizes) == g.bfs_trace(trial % 150)
+
+
+def test_cc_known_answers_and_seeded(ref, orc):
+    off, nbr = csr(4, T4_PAIRS)
+    assert orc.cc(4, off, nbr).tolist() == [0, 0, 0, 0]
+    off, nbr = csr(5, np.zeros((0, 2), np.uint32))
+    assert orc.cc(5, off, nbr).tolist() == [0, 1, 2, 3, 4]
+    for trial in range(25):
+        n, pairs = ref.er(200, 0.008, 900 + trial)
+        off, nbr = csr(n, pairs)
+        assert np.array_equal(orc.cc(n, off, nbr), ref.csr(n, off, nbr).cc())
+
+
+def test_pagerank_known_answers(ref, orc):
+    # test_algorithms.cpp:294-313
+    n, pairs = undirected(4, [(0, 1), (1, 2), (2, 3), (3, 0)], orc)
+    p = orc.pagerank(n, *csr(n, pairs), 0.85, 20, 1e-4)
+    assert np.allclose(p, 0.25, rtol=1e-12, atol=0)
+    q = orc.pagerank(4, *csr(4, T4_PAIRS), 0.85, 20, 1e-4)
+    assert q[2] > q[0] and q[2] > q[1] and q[2] > q[3] and abs(q.sum() - 1) < 1e-6
+    with pytest.raises(ValueError):
+        orc.pagerank(4, *csr(4, T4_PAIRS), 1.5, 20, 1e-4)
+    with pytest.raises(ValueError):
+        orc.pagerank(4, *csr(4, T4_PAIRS), 0.85, 20, 0.0)
+
+
+def test_pagerank_matches_reference(ref, orc):
+    for trial in range(15):
+        n, pairs = ref.er(150, 0.04, 2300 + trial)
+        off, nbr = csr(n, pairs)
+        g = ref.csr(n, off, nbr)
+        for tol in (1e-4, TINY):
+            a = orc.pagerank(n, off, nbr, 0.85, 20, tol)
+            b = g.pagerank(0.85, 20, tol)
+            assert np.abs(a - b).sum() <= 1e-12
+
+
+def test_tc_known_answers(orc):
+    off, nbr = csr(4, T4_PAIRS)
+    assert orc.tc(4, off, nbr) == 1
+    for k in (3, 5, 8, 12):
+        n, pairs = undirected(k, complete(k), orc)
+        assert orc.tc(n, *csr(n, pairs)) == k * (k - 1) * (k - 2) // 6
+    n, pairs = undirected(50, star(49), orc)
+    assert orc.tc(n, *csr(n, pairs)) == 0
+    n, pairs = undirected(7, [(0, 1), (1, 2), (1, 3), (3, 4), (3, 5), (5, 6)], orc)  # tree
+    assert orc.tc(n, *csr(n, pairs)) == 0
+
+
+def test_tc_brute_force_small(ref, orc):
+    for trial in range(10):
+        n, pairs = ref.er(40, 0.2, 77 + trial)
+        adj = np.zeros((n, n), dtype=np.int64)
+        adj[pairs[:, 0], pairs[:, 1]] = 1
+        brute = int(np.trace(adj @ adj @ adj)) // 6
+        assert orc.tc(n, *csr(n, pairs)) == brute
+
+
+def test_s16_outputs_match_golden(orc):
+    gd = golden(16)
+    n, pairs = orc.rmat(16, 16 << 16, 1)
+    off, nbr = csr(n, pairs)
+    src = max_degree_source(off)
+    assert src == gd["bfs"]["source"]
+    d, modes, sizes = orc.bfs(n, off, nbr, src)
+    assert digest(d) == gd["bfs"]["digest"]
+    assert modes == gd["bfs"]["modes"] and sizes == gd["bfs"]["frontier_sizes"]
+    assert digest(orc.cc(n, off, nbr)) == gd["cc"]["digest"]
+    p = orc.pagerank(n, off, nbr, 0.85, 20, TINY)
+    ids = np.array(gd["pagerank"]["sample_ids"])
+    want = np.array([float.fromhex(h) for h in gd["pagerank"]["sample_hex"]])
+    assert np.abs(p[ids] - want).max() <= 1e-15
+    assert orc.tc(n, off, nbr) == gd["tc"]["triangles"]
+
+
+# ---------------------------------------------------------------- batches
+def test_prepare_global_known_answers(ref, orc):
+    # test_batch.cpp:25-30, 50-62
+    raw = [[2, 3], [0, 1], [2, 1], [0, 1]]
+    assert orc.prepare_global(raw).tolist() == [[0, 1], [2, 1], [2, 3]]
+    assert ref.prepare_global(raw).tolist() == [[0, 1], [2, 1], [2, 3]]
+    loops = [[1, 1], [2, 2], [1, 2], [1, 2], [2, 1]]
+    assert orc.prepare_global(loops).tolist() == [[1, 2], [2, 1]]
+    assert orc.prepare_global(np.zeros((0, 2), np.uint32)).shape[0] == 0
+
+
+def test_set_apply_t4_counts(orc):
+    # test_batch.cpp:85-125
+    off, nbr = csr(4, T4_PAIRS)
+    add = orc.prepare_global([[0, 3], [3, 0]])
+    k, off, nbr = orc.set_apply(4, off, nbr, add, True)
+    assert k == 2 and int(off[4]) == 10 and int(off[4] - off[3]) == 2
+    k, off, nbr = orc.set_apply(4, off, nbr, orc.prepare_global(T4_PAIRS), True)
+    assert k == 0 and int(off[4]) == 10
+    k, off, nbr = orc.set_apply(4, off, nbr, add, False)
+    assert k == 2 and int(off[4]) == 8
+    t_off, t_nbr = csr(4, T4_PAIRS)
+    assert np.array_equal(off, t_off) and np.array_equal(nbr, t_nbr)
+    k, off, nbr = orc.set_apply(4, off, nbr, orc.prepare_global([[1, 3], [3, 1]]), False)
+    assert k == 0
+    k, off, nbr = orc.set_apply(4, off, nbr, orc.prepare_global([[2, 3], [3, 2]]), False)
+    assert k == 2 and int(off[4]) == 6
+    k, off, nbr = orc.set_apply(4, off, nbr, orc.prepare_global(T4_PAIRS), False)
+    assert int(off[4]) == 0 and off.size == 5
+
+
+def test_set_apply_matches_chunked_set(ref, orc):
+    # acceptance.cpp:272-320 shape: base-disjoint batch with duplicates
+    n, base = ref.rmat(14, 1 << 16, 11, 0.5, 0.1, 0.1)
+    off, nbr = csr(n, base)
+    raw = ref.update_batch(14, 20000, 777, 0.5, 0.1, 0.1)
+    keys = set(map(tuple, base.tolist()))
+    batch = np.array([e for e in raw.tolist() if tuple(e) not in keys], dtype=np.uint32)
+    batch = np.concatenate([batch, batch[: len(batch) // 2]])
+    c = ref.chunked(n, base)
+    ins = c.apply(batch, True)
+    k, o2, n2 = orc.set_apply(n, off, nbr, orc.prepare_global(batch), True)
+    assert k == ins > 0
+    eo, en = c.export()
+    assert np.array_equal(eo, o2) and np.array_equal(en, n2)
+    dele = c.apply(batch, False)
+    k2, o3, n3 = orc.set_apply(n, o2, n2, orc.prepare_global(batch), False)
+    assert k2 == dele == ins
+    assert np.array_equal(o3, off) and np.array_equal(n3, nbr)
