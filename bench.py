@@ -42,6 +42,11 @@ TINY = float(np.finfo(np.float64).tiny)
 METRIC = "PageRank GTEPS (20 fixed fp64 iterations, 20*m/t)"
 UNIT = "GTEPS"
 L2_BYTES = 126 * 2**20
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 # ---------------------------------------------------------------- plumbing
@@ -222,27 +227,27 @@ def run_updates(torch, gbg, S, steps, warmup, sizes):
     deleted (timed).  Throughput = sampled batch size / seconds
     (bench.hpp:72-74).  Batches are device-resident before timing."""
     g = gbg.generate_rmat(S, 16 << S, 1, *RMAT, kind=gbg.KIND_BLOCKED)
-    off, nbr = g.to_csr()
     n = g.num_vertices()
-    src_of = np.repeat(np.arange(n, dtype=np.uint64), np.diff(off.astype(np.int64)))
-    base_keys = (src_of << np.uint64(32)) | nbr.astype(np.uint64)
-    del src_of
+    src = int(np.argmax(g.degrees()))
+    depth = torch.empty(n, dtype=torch.int32, device="cuda")
     res = {}
     for size in sizes:
         buf = torch.empty(4 * size, dtype=torch.int32, device="cuda")
         seed = _hash_combine(_hash_combine(2, size), 0)
         gbg.generate_update_batch_device(S, size, seed, buf.data_ptr(), *RMAT)
-        raw = buf.cpu().numpy().view(np.uint32).reshape(-1, 2)
-        keys = (raw[:, 0].astype(np.uint64) << np.uint64(32)) | raw[:, 1].astype(np.uint64)
-        fresh = np.ascontiguousarray(raw[~np.isin(keys, base_keys)])
-        dev = torch.from_numpy(fresh.view(np.int32)).cuda()
-        cnt = fresh.shape[0]
+        present = torch.empty(2 * size, dtype=torch.uint8, device="cuda")
+        g.contains_device(buf.data_ptr(), 2 * size, present.data_ptr())
+        dev = buf.view(-1, 2)[present == 0].contiguous()
+        cnt = dev.shape[0]
         ins_t, del_t, bfs_t, applied = [], [], [], 0
-        src = int(np.argmax(np.diff(off.astype(np.int64))))
+        box = {}
+
+        def ins():
+            box["a"] = g.insert_batch_device(dev.data_ptr(), cnt)
+
         for rep in range(warmup + steps):
-            ti = events_time(torch, g.stream(), lambda: res.__setitem__("_a", g.insert_batch_device(dev.data_ptr(), cnt)), 1)
-            applied = res.pop("_a")
-            depth = torch.empty(n, dtype=torch.int32, device="cuda")
+            ti = events_time(torch, g.stream(), ins, 1)
+            applied = box["a"]
             tb = events_time(torch, g.stream(), lambda: gbg.bfs_device(g, src, depth.data_ptr()), 1)
             td = events_time(torch, g.stream(), lambda: g.delete_batch_device(dev.data_ptr(), cnt), 1)
             if rep >= warmup:
@@ -364,6 +369,7 @@ def main():
     with Clocks(local) as clk:
         t_step, launches, pr_out = run_pagerank(torch, gbg, g, args.steps, args.warmup)
     t_max = max_over_ranks(t_step, world, device="cuda")
+    log(f"pagerank s{S}: {t_step * 1e3:.2f} ms/step")
     value = world * 20 * m / t_max / 1e9
     peaks, peak_src = measured_peaks()
     it_s = t_step / 20
@@ -400,6 +406,7 @@ def main():
            "ms_per_step": t_e2e * 1e3,
            "path": "gbg_csr_create (pinned host CSR -> device, validated) + gbg_pagerank (ranks -> host)"}
 
+    log(f"e2e: {t_e2e * 1e3:.1f} ms/step")
     workloads = {}
     if rank == 0 and not args.no_secondary:
         # configs[2]: DO-BFS + CC on the same scale-24 graph
@@ -445,12 +452,14 @@ def main():
         # configs[4]: updates on the blocked container at s22
         upd, _gb = run_updates(torch, gbg, 22, max(1, min(args.steps, 3)), 1, [10**4, 10**5, 10**6, 10**7])
         workloads["updates_s22"] = upd
+        log("secondary workloads done")
         del _gb
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cb = cpu_reference_pr(off, nbr, n, 1, 0)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        log(f"cpu baseline: {cb['seconds_per_step']:.2f} s/step, csr build {cb['container_build_s']:.1f} s")
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -185,6 +185,11 @@ gbg_status gbg_delete_batch_device(gbg_graph* g, const uint32_t* arcs_dev, uint6
  * GBG_ERR_INVALID_ARGUMENT (set_graph.hpp:147-148). */
 gbg_status gbg_insert_edge(gbg_graph* g, uint32_t src, uint32_t dst, int* changed);
 gbg_status gbg_delete_edge(gbg_graph* g, uint32_t src, uint32_t dst, int* changed);
+/* Arc membership for `count` device (src,dst) pairs: out_dev[i] = 1 iff the
+ * arc is present (ChunkedSortedSet::contains per source,
+ * neighbor_sets.hpp:305-310); out-of-range ids give 0.  Used to keep update
+ * batches disjoint from the base graph (bench.cpp:150-169). */
+gbg_status gbg_contains_device(gbg_graph* g, const uint32_t* arcs_dev, uint64_t count, uint8_t* out_dev);
 /* gb::generate_update_batch (batch.cpp:128-154) on the device, bit-exact:
  * writes 2*size (src,dst) pairs (draw, then its reverse) to arcs_dev. */
 gbg_status gbg_update_batch_device(uint32_t log2_n, double a, double b, double c, uint64_t size,

@@ -153,6 +153,24 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
   return lo;
 }
 
+// arc membership queries: out[i] = (src,dst) present (0 for out-of-range ids)
+template <class G>
+__global__ void contains_k(G g, const uint32_t* pairs, uint64_t count, uint8_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint32_t s = pairs[2 * i], d = pairs[2 * i + 1];
+    uint8_t r = 0;
+    if (s < g.n && d < g.n) {
+      uint64_t b;
+      uint32_t len;
+      g.seg(s, b, len);
+      const uint32_t pos = lower_bound_u32(g.data() + b, len, d);
+      r = pos < len && g.at(b + pos) == d;
+    }
+    out[i] = r;
+  }
+}
+
 // presence of each prepared arc in the container; keep those that change it
 struct ApplyIn {
   const uint64_t* k;
@@ -511,6 +529,19 @@ gbg_status gbg_insert_edge(gbg_graph* g, uint32_t src, uint32_t dst, int* change
 }
 gbg_status gbg_delete_edge(gbg_graph* g, uint32_t src, uint32_t dst, int* changed) {
   return single_arc(g, src, dst, changed, false);
+}
+
+gbg_status gbg_contains_device(gbg_graph* g, const uint32_t* arcs_dev, uint64_t count, uint8_t* out_dev) {
+  return guard([&] {
+    GBG_HANDLE(g);
+    if (count && (!arcs_dev || !out_dev)) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    if (!count) return;
+    with_view(g, [&](auto view) {
+      GBG_LAUNCH(g, contains_k<decltype(view)>, grid_for(count, 256, g->sm_count * 16), 256, 0, view, arcs_dev, count,
+                 out_dev);
+    });
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+  });
 }
 
 }  // extern "C"

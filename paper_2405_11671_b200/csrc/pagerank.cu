@@ -200,6 +200,13 @@ __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32
   if (a.p_out) a.p_out[v] = next;
 }
 
+constexpr int kPerThread = (kTileMax + kPrThreads - 1) / kPrThreads;  // 13
+
+// Persistent: CTA b owns work items b, b + grid, b + 2*grid, ... (a static
+// assignment, so the err / dangling fold below is deterministic).  Each
+// light tile issues all of its global loads (row ends, neighbour ids, then
+// the dependent contrib gathers) as unrolled batches before one barrier, so
+// every thread has ~kPerThread independent requests in flight per phase.
 template <class G>
 __global__ void __launch_bounds__(kPrThreads) pr_iter_k(G g, PrArgs a) {
   __shared__ double s_val[kTileMax];
@@ -209,15 +216,15 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(G g, PrArgs a) {
   __shared__ int s_flag;
 
   if (a.sc->done) return;
-  const uint32_t w = blockIdx.x;
-  const uint32_t t = a.work_tile[w];
-  const uint32_t r0 = a.tile_row[t], r1 = a.tile_row[t + 1];
   const double dcur = a.sc->dangling[a.iter & 1];
   const double base = (1.0 - a.damping) / a.nd + a.damping * dcur / a.nd;
   double err = 0.0, dang = 0.0;
 
-  const uint64_t eb = a.voff[r0];
-  const uint64_t d0 = a.voff[r0 + 1] - eb;
+  for (uint32_t w = blockIdx.x; w < a.nwork; w += gridDim.x) {
+  const uint32_t t = __ldg(a.work_tile + w);
+  const uint32_t r0 = __ldg(a.tile_row + t), r1 = __ldg(a.tile_row + t + 1);
+  const uint64_t eb = __ldg(a.voff + r0);
+  const uint64_t d0 = __ldg(a.voff + r0 + 1) - eb;
   if (r1 - r0 == 1 && d0 > kHeavy) {
     // ---- heavy row chunk
     const uint32_t c = a.work_chunk[w];
@@ -228,7 +235,19 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(G g, PrArgs a) {
     const uint64_t lo = static_cast<uint64_t>(c) * kChunk;
     const uint64_t hi = (d0 < lo + kChunk ? d0 : lo + kChunk);
     double acc = 0.0;
-    for (uint64_t k = lo + threadIdx.x; k < hi; k += kPrThreads) acc += fmax(a.x_old[g.at(b + k)], 0.0);
+    constexpr int kCh = kChunk / kPrThreads;  // 16 per thread
+    uint32_t ids[kCh];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      const uint64_t k = lo + threadIdx.x + j * kPrThreads;
+      ids[j] = k < hi ? g.at(b + k) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      const uint64_t k = lo + threadIdx.x + j * kPrThreads;
+      const double x = k < hi ? __ldg(a.x_old + ids[j]) : 0.0;
+      acc += fmax(x, 0.0);
+    }
     const double s = block_sum(acc, s_red);
     if (threadIdx.x == 0) {
       a.heavy_partial[w] = s;
@@ -247,14 +266,40 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(G g, PrArgs a) {
   } else {
     // ---- light tile: rows [r0, r1), edges [eb, eb+E)
     const uint32_t R = r1 - r0;
-    for (uint32_t i = threadIdx.x; i < R; i += kPrThreads)
-      s_rowend[i] = static_cast<uint32_t>(a.voff[r0 + i + 1] - eb);
-    __syncthreads();
-    const uint32_t E = s_rowend[R - 1];
+    const uint32_t E = static_cast<uint32_t>(__ldg(a.voff + r1) - eb);
+    uint64_t rend[kPerThread];
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      const uint32_t i = threadIdx.x + j * kPrThreads;
+      rend[j] = i < R ? __ldg(a.voff + r0 + i + 1) : 0;
+    }
     if (G::kContiguous) {
       const uint64_t b0 = g.seg_begin(r0);
-      for (uint32_t k = threadIdx.x; k < E; k += kPrThreads) s_val[k] = fmax(a.x_old[g.at(b0 + k)], 0.0);
-    } else {
+      uint32_t ids[kPerThread];
+#pragma unroll
+      for (int j = 0; j < kPerThread; ++j) {
+        const uint32_t k = threadIdx.x + j * kPrThreads;
+        ids[j] = k < E ? g.at(b0 + k) : 0u;
+      }
+      double xv[kPerThread];
+#pragma unroll
+      for (int j = 0; j < kPerThread; ++j) {
+        const uint32_t k = threadIdx.x + j * kPrThreads;
+        xv[j] = k < E ? __ldg(a.x_old + ids[j]) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kPerThread; ++j) {
+        const uint32_t k = threadIdx.x + j * kPrThreads;
+        if (k < E) s_val[k] = fmax(xv[j], 0.0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      const uint32_t i = threadIdx.x + j * kPrThreads;
+      if (i < R) s_rowend[i] = static_cast<uint32_t>(rend[j] - eb);
+    }
+    __syncthreads();
+    if (!G::kContiguous) {
       for (uint32_t k = threadIdx.x; k < E; k += kPrThreads) {
         uint32_t lo = 0, hi = R;  // first row with rowend > k
         while (lo < hi) {
@@ -325,22 +370,24 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(G g, PrArgs a) {
       pr_finalize(a, base, r0 + fr, deg, first_val, err, dang);
     }
   }
+  __syncthreads();  // shared tile buffers are reused by the next work item
+  }
   // ---- per-CTA partials, last CTA folds them in order
   const double be = block_sum(err, s_red);
   const double bd = block_sum(dang, s_red);
   if (threadIdx.x == 0) {
-    a.blk[2 * w] = be;
-    a.blk[2 * w + 1] = bd;
+    a.blk[2 * blockIdx.x] = be;
+    a.blk[2 * blockIdx.x + 1] = bd;
     __threadfence();
-    s_flag = atomicAdd(a.done_counter, 1u) == a.nwork - 1;
+    s_flag = atomicAdd(a.done_counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (s_flag) {
     __threadfence();
     double e = 0.0, dg = 0.0;
-    for (uint64_t k = threadIdx.x; k < a.nwork; k += kPrThreads) {
-      e += ((volatile double*)a.blk)[2 * k];
-      dg += ((volatile double*)a.blk)[2 * k + 1];
+    for (uint64_t k = threadIdx.x; k < gridDim.x; k += kPrThreads) {
+      e += __ldcg(a.blk + 2 * k);
+      dg += __ldcg(a.blk + 2 * k + 1);
     }
     e = block_sum(e, s_red);
     dg = block_sum(dg, s_red);
@@ -405,11 +452,14 @@ uint64_t pagerank_run(gbg_graph* g, G view, double damping, uint64_t max_iters, 
   device_scan<double>(g, DanglingIn<G>{view, p0}, NullOut{}, n, d0, "pr.dang");
   GBG_LAUNCH(g, pr_scalars_init_k, 1, 1, 0, sc, d0);
   double* X[2] = {X0, X1};
+  int per_sm = 1;
+  GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pr_iter_k<G>, kPrThreads, 0));
+  const uint64_t grid = std::min<uint64_t>(s->nwork, static_cast<uint64_t>(std::max(per_sm, 1)) * g->sm_count);
   for (uint64_t it = 0; it < max_iters; ++it) {
     PrArgs a{s->tile_row, s->work_tile, s->work_chunk, voff, X[it & 1], X[(it + 1) & 1],
              it + 1 == max_iters ? p_dev : nullptr, s->heavy_partial, s->heavy_counter, s->blk,
              s->done_counter, sc, s->nwork, damping, static_cast<double>(n), tol, static_cast<int>(it)};
-    GBG_LAUNCH(g, pr_iter_k<G>, static_cast<unsigned>(s->nwork), kPrThreads, 0, view, a);
+    GBG_LAUNCH(g, pr_iter_k<G>, static_cast<unsigned>(grid), kPrThreads, 0, view, a);
   }
   PrScalars hs;
   GBG_CUDA(cudaMemcpyAsync(g->hscalar, sc, sizeof(PrScalars), cudaMemcpyDeviceToHost, g->stream));

@@ -149,6 +149,7 @@ _SIGS = {
     "gbg_insert_edge": [_vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_int)],
     "gbg_delete_edge": [_vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_int)],
     "gbg_update_batch_device": [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _vp],
+    "gbg_contains_device": [_vp, _vp, C.c_uint64, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_L, _name)
@@ -278,6 +279,10 @@ class _Graph:
         applied = C.c_uint64()
         _check(_L.gbg_delete_batch_device(self._h, arcs_ptr, count, C.byref(applied)))
         return applied.value
+
+    def contains_device(self, arcs_ptr: int, count: int, out_ptr: int):
+        """out[i] = 1 iff arc i (device uint32 pairs) is present."""
+        _check(_L.gbg_contains_device(self._h, arcs_ptr, count, out_ptr))
 
     # ---- runtime
     def stream(self) -> int:
