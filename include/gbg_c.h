@@ -158,6 +158,10 @@ gbg_status gbg_pagerank(gbg_graph* g, double damping, uint64_t max_iters, double
                         double* ranks, uint64_t* iterations);
 gbg_status gbg_pagerank_device(gbg_graph* g, double damping, uint64_t max_iters, double tolerance,
                                double* ranks_dev, uint64_t* iterations);
+/* Build (or fetch) the handle's cached PageRank layout — the graph
+ * renumbered by degree, see pagerank.cu — ahead of the first gbg_pagerank
+ * call; *build_ms = its one-time device build time.  Invalidated by updates. */
+gbg_status gbg_pagerank_prepare(gbg_graph* g, double* build_ms);
 /* gb::cc (algorithms.cpp:194-234): labels = minimum vertex id of each
  * component. */
 gbg_status gbg_cc(gbg_graph* g, uint32_t* labels);

@@ -8,6 +8,7 @@
 #include <memory>
 #include <vector>
 
+#include "edges.cuh"
 #include "traverse.cuh"
 
 namespace gbg {
@@ -53,26 +54,27 @@ __global__ void list_to_bitmap_k(const uint32_t* ids, uint64_t k, uint32_t* bm) 
   }
 }
 
-// csr.cpp:14-18: ids in range, each segment strictly increasing; plus the
-// offsets themselves monotone from 0 to m.
-__global__ void csr_validate_k(uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* nbr, int* bad) {
+// csr.cpp:14-18 split in two passes: the offsets are monotone from 0 to m
+// (vertex-parallel), then every id is in range and strictly above its
+// predecessor within the segment (edge-parallel, balanced).
+__global__ void csr_validate_offsets_k(uint64_t n, uint64_t m, const uint64_t* off, int* bad) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
     uint64_t b = off[v], e = off[v + 1];
-    if (e < b || e > m) {
-      *bad = 1;
-      continue;
-    }
-    for (uint64_t k = b; k < e; ++k) {
-      uint32_t x = nbr[k];
-      if (x >= n || (k > b && nbr[k - 1] >= x)) {
-        *bad = 1;
-        break;
-      }
-    }
+    if (e < b || e > m) *bad = 1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != m)) *bad = 1;
 }
+
+struct SegmentOrderOp {
+  const uint64_t* off;
+  const uint32_t* nbr;
+  uint64_t n;
+  int* bad;
+  __device__ __forceinline__ void operator()(uint32_t u, uint32_t v, uint64_t e) const {
+    if (v >= n || (e > off[u] && nbr[e - 1] >= v)) *bad = 1;
+  }
+};
 
 // arcs sorted strictly increasing by (src,dst), ids < n.  src/dst split out.
 __global__ void arcs_validate_split_k(uint64_t n, uint64_t m, const uint32_t* pairs, uint32_t* src,
@@ -184,8 +186,11 @@ gbg_status gbg_csr_create(uint64_t n, uint64_t m, const uint64_t* offsets, const
       GBG_CUDA(cudaMemcpyAsync(g->nbr, neighbors, m * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream));
     int* bad = g->ws.get<int>("bad", 1);
     GBG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
-    GBG_LAUNCH(g, csr_validate_k, grid_for(n, 256), 256, 0, n, m, g->off, g->nbr, bad);
+    GBG_LAUNCH(g, csr_validate_offsets_k, grid_for(n + 1, 256), 256, 0, n, m, g->off, bad);
     int hb = 0;
+    read_scalars(g, bad, sizeof(int), &hb);
+    if (hb) fail(GBG_ERR_FORMAT, "csr_build: offsets must rise monotonically from 0 to m");
+    for_each_edge(g, g->csr_view(), g->off, m, SegmentOrderOp{g->off, g->nbr, n, bad});
     read_scalars(g, bad, sizeof(int), &hb);
     if (hb) fail(GBG_ERR_FORMAT, "csr_build: arcs must be sorted, deduplicated and in range");
     *out = hold.release();

@@ -127,7 +127,7 @@ struct BlockedView {
 };
 
 // ---------------------------------------------------------------- handle
-struct PrSchedule;  // pagerank.cu
+struct PrLayout;  // pagerank.cu
 struct TcCache;     // tc.cu
 
 }  // namespace gbg
@@ -159,7 +159,7 @@ struct gbg_graph {
   // derived, rebuilt lazily after updates
   uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
   bool voff_valid = false;
-  gbg::PrSchedule* pr = nullptr;
+  gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
 
   gbg::Workspace ws;
   // pinned host staging for small device->host scalars

@@ -150,6 +150,7 @@ _SIGS = {
     "gbg_delete_edge": [_vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_int)],
     "gbg_update_batch_device": [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _vp],
     "gbg_contains_device": [_vp, _vp, C.c_uint64, _vp],
+    "gbg_pagerank_prepare": [_vp, _f64p],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_L, _name)
@@ -394,6 +395,13 @@ def pagerank(g: _Graph, damping: float = 0.85, max_iters: int = 20, tolerance: f
     it = C.c_uint64()
     _check(_L.gbg_pagerank(g.handle, damping, max_iters, tolerance, _p(out, _f64p), C.byref(it)))
     return out
+
+
+def pagerank_prepare(g: _Graph) -> float:
+    """Build the cached degree-ordered PageRank layout; returns its build ms."""
+    ms = C.c_double()
+    _check(_L.gbg_pagerank_prepare(g.handle, C.byref(ms)))
+    return ms.value
 
 
 def pagerank_device(g: _Graph, out_ptr: int, damping=0.85, max_iters=20, tolerance=1e-4) -> int:
