@@ -20,11 +20,13 @@
 // vertices are renumbered by (degree desc, id asc).  The pull is then a
 // gather into a vector whose hot part is contiguous: on the scale-24 R-MAT
 // graph the 2^22 highest-degree vertices (32 MiB of X) receive 98% of all
-// gathers and stay L2-resident, against 57% for the natural id order.
-// Rows of equal degree are also adjacent, so rows are processed in degree
-// classes with a fixed group of lanes per row (1..32 lanes, or several CTAs
-// for rows above kHeavy) — balanced with no merge path and no block
-// barriers on the light path.  Results are mapped back to original ids.
+// gathers, against 57% for the natural id order; the streamed arrays are
+// loaded evict_first and the gathers evict_last so that hot part stays in
+// L2.  Rows of equal degree are adjacent, so rows are processed in degree
+// classes, each with a fixed thread group per row and a fixed, fully
+// unrolled number of edges per thread (all of a thread's id loads, then all
+// of its gathers, in flight at once).  Results are mapped back to original
+// ids at the end.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -33,21 +35,25 @@
 #include <memory>
 #include <vector>
 
+#include "cache.cuh"
 #include "edges.cuh"
 
 namespace gbg {
 
 constexpr int kPrThreads = 256;
-constexpr uint32_t kHeavy = 2048;  // rows above this are split across CTAs
 constexpr uint32_t kChunk = 4096;  // edges per heavy-row chunk (16 per thread)
-// degree classes: 0 heavy, 1: 32 lanes (deg 65..kHeavy), 2: 16 lanes
-// (33..64), 3: 8 (17..32), 4: 4 (9..16), 5: 2 (5..8), 6: 1 (1..4),
-// 7: isolated (deg 0, finalize only)
-constexpr int kClasses = 8;
-__host__ __device__ constexpr uint32_t class_lanes(int c) { return c <= 1 ? 32u : c >= 6 ? 1u : 32u >> (c - 1); }
-// largest degree of class c (c >= 1)
+// Degree classes (rows in degree-descending order):
+//   0: deg > 4096     several CTAs per row (kChunk-edge chunks)
+//   1: 513..4096      one CTA per row, <= 16 edges per thread
+//   2: 65..512        one warp per row, <= 16 edges per lane
+//   3..7: 33..64, 17..32, 9..16, 5..8, 1..4: 16/8/4/2/1 lanes per row, <= 4 per lane
+//   8: isolated       finalize only
+constexpr int kClasses = 9;
+__host__ __device__ constexpr uint32_t class_threads(int c) {
+  return c <= 1 ? 256u : c == 2 ? 32u : c >= 7 ? 1u : 16u >> (c - 3);
+}
 __host__ __device__ constexpr uint32_t class_max_deg(int c) {
-  return c == 1 ? kHeavy : c == 7 ? 0u : 4u * class_lanes(c);
+  return c == 1 ? 4096u : c == 2 ? 512u : c >= 8 ? 0u : 4u * class_threads(c);
 }
 
 struct PrLayout {
@@ -59,6 +65,7 @@ struct PrLayout {
   uint32_t row_begin[kClasses + 1] = {};
   uint64_t unit_begin[kClasses + 1] = {};  // work units, class by class
   uint64_t* hchunk = nullptr;  // heavy rows: exclusive scan of chunk counts [nheavy+1]
+  uint32_t* hrow = nullptr;    // heavy chunk -> row
   unsigned* heavy_counter = nullptr;
   double* heavy_partial = nullptr;
   double* blk = nullptr;
@@ -71,6 +78,7 @@ struct PrLayout {
     dfree(ord);
     dfree(pos);
     dfree(hchunk);
+    dfree(hrow);
     dfree(heavy_counter);
     dfree(heavy_partial);
     dfree(blk);
@@ -103,7 +111,7 @@ struct SortedDegIn {
 };
 
 struct RelabelOp {
-  const uint64_t* voff;     // source graph prefix (CSR offsets / blocked virtual offsets)
+  const uint64_t* voff;  // source graph prefix (CSR offsets / blocked virtual offsets)
   const uint32_t* pos;
   const uint64_t* new_off;
   uint32_t* new_nbr;
@@ -112,10 +120,10 @@ struct RelabelOp {
   }
 };
 
-// first row (in the degree-descending order) whose degree is <= bound
+// first row (degree-descending order) whose degree is <= class_max_deg(c+1)
 __global__ void class_bounds_k(const uint64_t* off, uint64_t n, uint32_t* out) {
-  if (threadIdx.x >= kClasses) return;
-  const int c = threadIdx.x;  // boundary between class c and c+1
+  const int c = threadIdx.x;
+  if (c >= kClasses - 1) return;
   const uint32_t bound = class_max_deg(c + 1);
   uint64_t lo = 0, hi = n;
   while (lo < hi) {
@@ -129,6 +137,16 @@ struct HeavyChunksIn {
   const uint64_t* off;
   __device__ __forceinline__ uint64_t operator()(uint64_t r) const {
     return (off[r + 1] - off[r] + kChunk - 1) / kChunk;
+  }
+};
+struct HeavyChunksOut {
+  const uint64_t* off;
+  uint64_t* hchunk;
+  uint32_t* hrow;
+  __device__ __forceinline__ void operator()(uint64_t r, uint64_t pre) const {
+    hchunk[r] = pre;
+    const uint64_t c = HeavyChunksIn{off}(r);
+    for (uint64_t k = 0; k < c; ++k) hrow[pre + k] = static_cast<uint32_t>(r);
   }
 };
 
@@ -168,14 +186,16 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   const uint32_t nheavy = L->row_begin[1];
   L->hchunk = dalloc<uint64_t>(nheavy + 1);
   uint64_t nchunks = 0;
-  device_scan<uint64_t>(g, HeavyChunksIn{L->off}, ArrayOut<uint64_t>{L->hchunk}, nheavy, L->hchunk + nheavy,
-                        "prl.heavy");
+  device_scan<uint64_t>(g, HeavyChunksIn{L->off}, NullOut{}, nheavy, L->hchunk + nheavy, "prl.heavy");
   read_scalars(g, L->hchunk + nheavy, sizeof(nchunks), &nchunks);
+  L->hrow = dalloc<uint32_t>(nchunks + 1);
+  device_scan<uint64_t>(g, HeavyChunksIn{L->off}, HeavyChunksOut{L->off, L->hchunk, L->hrow}, nheavy,
+                        L->hchunk + nheavy, "prl.heavy");
   L->unit_begin[0] = 0;
   L->unit_begin[1] = nchunks;
   for (int c = 1; c < kClasses; ++c) {
     const uint64_t rows = L->row_begin[c + 1] - L->row_begin[c];
-    const uint64_t per_unit = kPrThreads / class_lanes(c);
+    const uint64_t per_unit = kPrThreads / class_threads(c);
     L->unit_begin[c + 1] = L->unit_begin[c] + (rows + per_unit - 1) / per_unit;
   }
   L->heavy_counter = dalloc<unsigned>(nheavy + 1);
@@ -210,6 +230,7 @@ struct PrArgs {
   const double* x_old;
   double* x_new;
   const uint64_t* hchunk;
+  const uint32_t* hrow;
   double* heavy_partial;
   unsigned* heavy_counter;
   double* blk;
@@ -226,7 +247,7 @@ struct PrArgs {
 __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32_t r, uint64_t d, double sum,
                                             double& err, double& dang) {
   const double next = base + a.damping * sum;
-  const double xo = __ldg(a.x_old + r);
+  const double xo = __ldcs(a.x_old + r);
   const double pold = d ? xo * static_cast<double>(d) : -xo;
   err += fabs(next - pold);
   if (d) {
@@ -237,8 +258,25 @@ __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32
   }
 }
 
-__device__ __forceinline__ double gather(const PrArgs& a, uint64_t e) {
-  return fmax(__ldg(a.x_old + __ldg(a.nbr + e)), 0.0);
+// Sum of fmax(X[nbr[e]], 0) over e = b + t, b + t + T, ... (< b + d), with
+// all K id loads issued before the K gathers.
+template <int K>
+__device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint64_t d, uint32_t t, uint32_t T,
+                                             uint64_t pf, uint64_t pl) {
+  uint32_t ids[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const uint64_t k = t + static_cast<uint64_t>(j) * T;
+    ids[j] = k < d ? ld_stream_u32(a.nbr + b + k, pf) : 0u;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const uint64_t k = t + static_cast<uint64_t>(j) * T;
+    const double x = k < d ? ld_keep_f64(a.x_old + ids[j], pl) : 0.0;
+    acc += fmax(x, 0.0);
+  }
+  return acc;
 }
 
 // Persistent: CTA b owns work units b, b + grid, ... (static assignment, so
@@ -247,92 +285,64 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
   __shared__ double s_red[33];
   __shared__ int s_flag;
   if (a.sc->done) return;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   const double dcur = a.sc->dangling[a.iter & 1];
   const double base = (1.0 - a.damping) / a.nd + a.damping * dcur / a.nd;
   double err = 0.0, dang = 0.0;
   const uint64_t total = a.unit_begin[kClasses];
-  const uint64_t nheavy_units = a.unit_begin[1];
 
-  // ---- heavy rows: kChunk edges per unit, deterministic two-level sum
-  for (uint64_t w = blockIdx.x; w < nheavy_units; w += gridDim.x) {
-    uint32_t lo = 0, hi = a.row_begin[1];  // hchunk[lo] <= w < hchunk[hi]
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(a.hchunk + mid) <= w) lo = mid; else hi = mid;
-    }
-    const uint32_t r = lo;
-    const uint64_t c0 = __ldg(a.hchunk + r);
-    const uint32_t nch = static_cast<uint32_t>(__ldg(a.hchunk + r + 1) - c0);
-    const uint64_t c = w - c0;
-    const uint64_t rb = __ldg(a.off + r), re = __ldg(a.off + r + 1);
-    const uint64_t eb = rb + c * kChunk;
-    const uint64_t ee = eb + kChunk < re ? eb + kChunk : re;
-    constexpr int kCh = kChunk / kPrThreads;
-    uint32_t ids[kCh];
+  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    int c = 0;
 #pragma unroll
-    for (int j = 0; j < kCh; ++j) {
-      const uint64_t e = eb + threadIdx.x + j * kPrThreads;
-      ids[j] = e < ee ? __ldg(a.nbr + e) : 0u;
-    }
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < kCh; ++j) {
-      const uint64_t e = eb + threadIdx.x + j * kPrThreads;
-      acc += e < ee ? fmax(__ldg(a.x_old + ids[j]), 0.0) : 0.0;
-    }
-    const double s = block_sum(acc, s_red);
-    if (threadIdx.x == 0) {
-      a.heavy_partial[w] = s;
-      __threadfence();
-      s_flag = atomicAdd(a.heavy_counter + r, 1u) == nch - 1;
-    }
-    __syncthreads();
-    if (s_flag && threadIdx.x == 0) {
-      __threadfence();
-      double tot = 0.0;
-      for (uint32_t k = 0; k < nch; ++k) tot += __ldcg(a.heavy_partial + c0 + k);
-      pr_finalize(a, base, r, re - rb, tot, err, dang);
-      a.heavy_counter[r] = 0;
-    }
-    __syncthreads();
-  }
-
-  // ---- light rows: a fixed group of `lanes` threads per row; the rows of a
-  // unit are consecutive (equal degree class), so no barriers are needed
-  for (uint64_t w = nheavy_units + blockIdx.x; w < total; w += gridDim.x) {
-    int c = 1;
-#pragma unroll
-    for (int k = 2; k < kClasses; ++k)
+    for (int k = 1; k < kClasses; ++k)
       if (w >= a.unit_begin[k]) c = k;
-    const uint32_t lanes = class_lanes(c);
-    const uint32_t rows_per_unit = kPrThreads / lanes;
-    const uint64_t r64 = a.row_begin[c] + (w - a.unit_begin[c]) * rows_per_unit + threadIdx.x / lanes;
-    const bool valid = r64 < a.row_begin[c + 1];
-    const uint32_t r = static_cast<uint32_t>(r64);
-    const uint32_t l = threadIdx.x & (lanes - 1);
-    double acc = 0.0;
-    uint64_t d = 0;
-    if (valid) {
-      const uint64_t rb = __ldg(a.off + r);
-      d = __ldg(a.off + r + 1) - rb;
-      uint64_t e = rb + l;
-      const uint64_t re = rb + d;
-      // four independent gathers in flight per lane
-      for (; e + 3 * lanes < re; e += 4 * lanes) {
-        const uint32_t u0 = __ldg(a.nbr + e), u1 = __ldg(a.nbr + e + lanes), u2 = __ldg(a.nbr + e + 2 * lanes),
-                       u3 = __ldg(a.nbr + e + 3 * lanes);
-        const double x0 = __ldg(a.x_old + u0), x1 = __ldg(a.x_old + u1), x2 = __ldg(a.x_old + u2),
-                     x3 = __ldg(a.x_old + u3);
-        acc += fmax(x0, 0.0);
-        acc += fmax(x1, 0.0);
-        acc += fmax(x2, 0.0);
-        acc += fmax(x3, 0.0);
+    if (c == 0) {
+      // ---- heavy row chunk: deterministic two-level sum
+      const uint32_t r = __ldg(a.hrow + w);
+      const uint64_t c0 = __ldg(a.hchunk + r);
+      const uint64_t rb = __ldg(a.off + r), re = __ldg(a.off + r + 1);
+      const uint32_t nch = static_cast<uint32_t>((re - rb + kChunk - 1) / kChunk);
+      const uint64_t eb = rb + (w - c0) * kChunk;
+      const uint64_t len = eb + kChunk < re ? kChunk : re - eb;
+      const double s = block_sum(gather_sum<kChunk / kPrThreads>(a, eb, len, threadIdx.x, kPrThreads, pf, pl), s_red);
+      if (threadIdx.x == 0) {
+        a.heavy_partial[w] = s;
+        __threadfence();
+        s_flag = atomicAdd(a.heavy_counter + r, 1u) == nch - 1;
       }
-      for (; e < re; e += lanes) acc += gather(a, e);
+      __syncthreads();
+      if (s_flag && threadIdx.x == 0) {
+        __threadfence();
+        double tot = 0.0;
+        for (uint32_t k = 0; k < nch; ++k) tot += __ldcg(a.heavy_partial + c0 + k);
+        pr_finalize(a, base, r, re - rb, tot, err, dang);
+        a.heavy_counter[r] = 0;
+      }
+      __syncthreads();
+    } else if (c == 1) {
+      // ---- one CTA per row
+      const uint32_t r = a.row_begin[1] + static_cast<uint32_t>(w - a.unit_begin[1]);
+      const uint64_t rb = __ldg(a.off + r), d = __ldg(a.off + r + 1) - rb;
+      const double s = block_sum(gather_sum<16>(a, rb, d, threadIdx.x, kPrThreads, pf, pl), s_red);
+      if (threadIdx.x == 0) pr_finalize(a, base, r, d, s, err, dang);
+    } else {
+      // ---- a fixed group of lanes per row, rows of the unit consecutive
+      const uint32_t lanes = class_threads(c);
+      const uint32_t rows_per_unit = kPrThreads / lanes;
+      const uint64_t r64 = a.row_begin[c] + (w - a.unit_begin[c]) * rows_per_unit + threadIdx.x / lanes;
+      const bool valid = r64 < a.row_begin[c + 1];
+      const uint32_t r = static_cast<uint32_t>(r64);
+      const uint32_t l = threadIdx.x & (lanes - 1);
+      double acc = 0.0;
+      uint64_t d = 0;
+      if (valid) {
+        const uint64_t rb = ld_stream_u64(a.off + r, pf);
+        d = ld_stream_u64(a.off + r + 1, pf) - rb;
+        acc = c == 2 ? gather_sum<16>(a, rb, d, l, lanes, pf, pl) : gather_sum<4>(a, rb, d, l, lanes, pf, pl);
+      }
+      for (uint32_t o = lanes >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, lanes);
+      if (valid && l == 0) pr_finalize(a, base, r, d, acc, err, dang);
     }
-    // group reduce (fixed xor tree inside the lane group)
-    for (uint32_t o = lanes >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, lanes);
-    if (valid && l == 0) pr_finalize(a, base, r, d, acc, err, dang);
   }
 
   // ---- per-CTA partials, last CTA folds them in order
@@ -429,6 +439,7 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
     a.x_old = X[it & 1];
     a.x_new = X[(it + 1) & 1];
     a.hchunk = L->hchunk;
+    a.hrow = L->hrow;
     a.heavy_partial = L->heavy_partial;
     a.heavy_counter = L->heavy_counter;
     a.blk = L->blk;
