@@ -42,19 +42,21 @@ namespace gbg {
 
 constexpr int kPrThreads = 256;
 constexpr uint32_t kChunk = 4096;  // edges per heavy-row chunk (16 per thread)
-// Degree classes (rows in degree-descending order):
-//   0: deg > 4096     several CTAs per row (kChunk-edge chunks)
-//   1: 513..4096      one CTA per row, <= 16 edges per thread
-//   2: 65..512        one warp per row, <= 16 edges per lane
-//   3..7: 33..64, 17..32, 9..16, 5..8, 1..4: 16/8/4/2/1 lanes per row, <= 4 per lane
-//   8: isolated       finalize only
-constexpr int kClasses = 9;
+// Degree classes over the degree-descending rows: class c gives each row
+// T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
+// at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
+// 4096) splits rows into kChunk-edge chunks across CTAs; the last class is
+// the isolated rows (finalize only).
+constexpr int kClasses = 15;
 __host__ __device__ constexpr uint32_t class_threads(int c) {
-  return c <= 1 ? 256u : c == 2 ? 32u : c >= 7 ? 1u : 16u >> (c - 3);
+  constexpr uint32_t t[kClasses] = {256, 256, 256, 256, 32, 32, 32, 16, 8, 4, 2, 1, 1, 1, 1};
+  return t[c];
 }
-__host__ __device__ constexpr uint32_t class_max_deg(int c) {
-  return c == 1 ? 4096u : c == 2 ? 512u : c >= 8 ? 0u : 4u * class_threads(c);
+__host__ __device__ constexpr uint32_t class_k(int c) {
+  constexpr uint32_t k[kClasses] = {16, 16, 8, 4, 16, 8, 4, 4, 4, 4, 4, 4, 2, 1, 0};
+  return k[c];
 }
+__host__ __device__ constexpr uint32_t class_max_deg(int c) { return c == 0 ? 0xffffffffu : class_threads(c) * class_k(c); }
 
 struct PrLayout {
   uint64_t n = 0, m = 0;
@@ -319,11 +321,15 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
         a.heavy_counter[r] = 0;
       }
       __syncthreads();
-    } else if (c == 1) {
+    } else if (c <= 3) {
       // ---- one CTA per row
-      const uint32_t r = a.row_begin[1] + static_cast<uint32_t>(w - a.unit_begin[1]);
+      const uint32_t r = a.row_begin[c] + static_cast<uint32_t>(w - a.unit_begin[c]);
       const uint64_t rb = __ldg(a.off + r), d = __ldg(a.off + r + 1) - rb;
-      const double s = block_sum(gather_sum<16>(a, rb, d, threadIdx.x, kPrThreads, pf, pl), s_red);
+      double p;
+      if (c == 1) p = gather_sum<16>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      else if (c == 2) p = gather_sum<8>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      else p = gather_sum<4>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      const double s = block_sum(p, s_red);
       if (threadIdx.x == 0) pr_finalize(a, base, r, d, s, err, dang);
     } else {
       // ---- a fixed group of lanes per row, rows of the unit consecutive
@@ -338,7 +344,14 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
       if (valid) {
         const uint64_t rb = ld_stream_u64(a.off + r, pf);
         d = ld_stream_u64(a.off + r + 1, pf) - rb;
-        acc = c == 2 ? gather_sum<16>(a, rb, d, l, lanes, pf, pl) : gather_sum<4>(a, rb, d, l, lanes, pf, pl);
+        switch (class_k(c)) {
+          case 16: acc = gather_sum<16>(a, rb, d, l, lanes, pf, pl); break;
+          case 8: acc = gather_sum<8>(a, rb, d, l, lanes, pf, pl); break;
+          case 4: acc = gather_sum<4>(a, rb, d, l, lanes, pf, pl); break;
+          case 2: acc = gather_sum<2>(a, rb, d, l, lanes, pf, pl); break;
+          case 1: acc = gather_sum<1>(a, rb, d, l, lanes, pf, pl); break;
+          default: break;
+        }
       }
       for (uint32_t o = lanes >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, lanes);
       if (valid && l == 0) pr_finalize(a, base, r, d, acc, err, dang);
