@@ -40,9 +40,8 @@
 
 namespace gbg {
 
-constexpr int kPrThreads = 1024;
-constexpr uint32_t kChunk = 8192;    // edges per heavy-row chunk (8 per thread)
-constexpr uint32_t kHotMax = 24576;  // contribs kept in shared memory (192 KiB)
+constexpr int kPrThreads = 256;
+constexpr uint32_t kChunk = 4096;  // edges per heavy-row chunk (16 per thread)
 // Degree classes over the degree-descending rows: class c gives each row
 // T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
 // at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
@@ -50,11 +49,11 @@ constexpr uint32_t kHotMax = 24576;  // contribs kept in shared memory (192 KiB)
 // the isolated rows (finalize only).
 constexpr int kClasses = 15;
 __host__ __device__ constexpr uint32_t class_threads(int c) {
-  constexpr uint32_t t[kClasses] = {1024, 256, 256, 256, 32, 32, 32, 16, 8, 4, 2, 1, 1, 1, 1};
+  constexpr uint32_t t[kClasses] = {256, 256, 256, 256, 32, 32, 32, 16, 8, 4, 2, 1, 1, 1, 1};
   return t[c];
 }
 __host__ __device__ constexpr uint32_t class_k(int c) {
-  constexpr uint32_t k[kClasses] = {8, 16, 8, 4, 16, 8, 4, 4, 4, 4, 4, 4, 2, 1, 0};
+  constexpr uint32_t k[kClasses] = {16, 16, 8, 4, 16, 8, 4, 4, 4, 4, 4, 4, 2, 1, 0};
   return k[c];
 }
 __host__ __device__ constexpr uint32_t class_max_deg(int c) { return c == 0 ? 0xffffffffu : class_threads(c) * class_k(c); }
@@ -74,7 +73,6 @@ struct PrLayout {
   double* blk = nullptr;
   unsigned* done_counter = nullptr;
   uint32_t grid = 0;
-  uint32_t hot = 0;
   double build_ms = 0;
   ~PrLayout() {
     dfree(off);
@@ -244,7 +242,6 @@ struct PrArgs {
   uint64_t unit_begin[kClasses + 1];
   double damping, nd, tol;
   int iter;
-  uint32_t hot;  // contribs of rows [0, hot) served from shared memory
 };
 
 // Finalize row r (algorithms.cpp:544-550 for one vertex) and emit the next
@@ -263,63 +260,38 @@ __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32
   }
 }
 
-// Sum of contrib[nbr[e]] over e = b + t, b + t + T, ... (< b + d), with all
-// K id loads issued before the K gathers.  Contribs of the `hot` highest-
-// degree vertices (new ids < hot) come from the shared-memory copy: random
-// 8-byte gathers are bound by L1TEX wavefronts (one line per cycle per SM),
-// and shared memory serves them several times faster.
+// Sum of fmax(X[nbr[e]], 0) over e = b + t, b + t + T, ... (< b + d), with
+// all K id loads issued before the K gathers.
 template <int K>
-__device__ __forceinline__ double gather_sum(const PrArgs& a, const double* s_hot, uint64_t b, uint64_t d,
-                                             uint32_t t, uint32_t T, uint64_t pf, uint64_t pl) {
+__device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint64_t d, uint32_t t, uint32_t T,
+                                             uint64_t pf, uint64_t pl) {
   uint32_t ids[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const uint64_t k = t + static_cast<uint64_t>(j) * T;
-    ids[j] = k < d ? ld_stream_u32(a.nbr + b + k, pf) : 0xffffffffu;
+    ids[j] = k < d ? ld_stream_u32(a.nbr + b + k, pf) : 0u;
   }
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    const uint32_t u = ids[j];
-    double x = 0.0;
-    if (u < a.hot) x = s_hot[u];
-    else if (u != 0xffffffffu) x = fmax(ld_keep_f64(a.x_old + u, pl), 0.0);
-    acc += x;
+    const uint64_t k = t + static_cast<uint64_t>(j) * T;
+    const double x = k < d ? ld_keep_f64(a.x_old + ids[j], pl) : 0.0;
+    acc += fmax(x, 0.0);
   }
   return acc;
 }
 
-// Sum over a 256-thread subgroup (8 warps), fixed order; result valid in
-// the subgroup's thread 0.  `buf` alternates between calls so a subgroup
-// may run one unit ahead without a second barrier.
-__device__ __forceinline__ double subgroup_sum(double v, double* s_part, int buf) {
-  v = warp_sum(v);
-  const int warp = threadIdx.x >> 5, sub = threadIdx.x >> 8;
-  if ((threadIdx.x & 31) == 0) s_part[buf * 32 + warp] = v;
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "r"(256) : "memory");
-  double s = 0.0;
-  if ((threadIdx.x & 255) == 0)
-    for (int k = 0; k < 8; ++k) s += s_part[buf * 32 + sub * 8 + k];
-  return s;
-}
-
-// Persistent, one CTA of 1024 threads per SM: CTA b owns work units b,
-// b + grid, ... (static assignment, so the err / dangling fold is
-// deterministic).
+// Persistent: CTA b owns work units b, b + grid, ... (static assignment, so
+// the err / dangling fold is deterministic).
 __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
-  extern __shared__ double s_hot[];
   __shared__ double s_red[33];
-  __shared__ double s_part[64];
   __shared__ int s_flag;
   if (a.sc->done) return;
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-  for (uint32_t i = threadIdx.x; i < a.hot; i += kPrThreads) s_hot[i] = fmax(ld_keep_f64(a.x_old + i, pl), 0.0);
-  __syncthreads();
   const double dcur = a.sc->dangling[a.iter & 1];
   const double base = (1.0 - a.damping) / a.nd + a.damping * dcur / a.nd;
   double err = 0.0, dang = 0.0;
   const uint64_t total = a.unit_begin[kClasses];
-  int parity = 0;
 
   for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
     int c = 0;
@@ -334,8 +306,7 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
       const uint32_t nch = static_cast<uint32_t>((re - rb + kChunk - 1) / kChunk);
       const uint64_t eb = rb + (w - c0) * kChunk;
       const uint64_t len = eb + kChunk < re ? kChunk : re - eb;
-      const double s =
-          block_sum(gather_sum<kChunk / kPrThreads>(a, s_hot, eb, len, threadIdx.x, kPrThreads, pf, pl), s_red);
+      const double s = block_sum(gather_sum<kChunk / kPrThreads>(a, eb, len, threadIdx.x, kPrThreads, pf, pl), s_red);
       if (threadIdx.x == 0) {
         a.heavy_partial[w] = s;
         __threadfence();
@@ -351,23 +322,15 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
       }
       __syncthreads();
     } else if (c <= 3) {
-      // ---- one 256-thread subgroup per row, four rows per unit
-      const uint64_t r64 = a.row_begin[c] + (w - a.unit_begin[c]) * (kPrThreads / 256) + (threadIdx.x >> 8);
-      const bool valid = r64 < a.row_begin[c + 1];
-      const uint32_t r = static_cast<uint32_t>(r64);
-      double p = 0.0;
-      uint64_t d = 0;
-      if (valid) {
-        const uint64_t rb = __ldg(a.off + r);
-        d = __ldg(a.off + r + 1) - rb;
-        const uint32_t t = threadIdx.x & 255;
-        if (c == 1) p = gather_sum<16>(a, s_hot, rb, d, t, 256, pf, pl);
-        else if (c == 2) p = gather_sum<8>(a, s_hot, rb, d, t, 256, pf, pl);
-        else p = gather_sum<4>(a, s_hot, rb, d, t, 256, pf, pl);
-      }
-      const double s = subgroup_sum(p, s_part, parity);
-      parity ^= 1;
-      if (valid && (threadIdx.x & 255) == 0) pr_finalize(a, base, r, d, s, err, dang);
+      // ---- one CTA per row
+      const uint32_t r = a.row_begin[c] + static_cast<uint32_t>(w - a.unit_begin[c]);
+      const uint64_t rb = __ldg(a.off + r), d = __ldg(a.off + r + 1) - rb;
+      double p;
+      if (c == 1) p = gather_sum<16>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      else if (c == 2) p = gather_sum<8>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      else p = gather_sum<4>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      const double s = block_sum(p, s_red);
+      if (threadIdx.x == 0) pr_finalize(a, base, r, d, s, err, dang);
     } else {
       // ---- a fixed group of lanes per row, rows of the unit consecutive
       const uint32_t lanes = class_threads(c);
@@ -382,11 +345,11 @@ __global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
         const uint64_t rb = ld_stream_u64(a.off + r, pf);
         d = ld_stream_u64(a.off + r + 1, pf) - rb;
         switch (class_k(c)) {
-          case 16: acc = gather_sum<16>(a, s_hot, rb, d, l, lanes, pf, pl); break;
-          case 8: acc = gather_sum<8>(a, s_hot, rb, d, l, lanes, pf, pl); break;
-          case 4: acc = gather_sum<4>(a, s_hot, rb, d, l, lanes, pf, pl); break;
-          case 2: acc = gather_sum<2>(a, s_hot, rb, d, l, lanes, pf, pl); break;
-          case 1: acc = gather_sum<1>(a, s_hot, rb, d, l, lanes, pf, pl); break;
+          case 16: acc = gather_sum<16>(a, rb, d, l, lanes, pf, pl); break;
+          case 8: acc = gather_sum<8>(a, rb, d, l, lanes, pf, pl); break;
+          case 4: acc = gather_sum<4>(a, rb, d, l, lanes, pf, pl); break;
+          case 2: acc = gather_sum<2>(a, rb, d, l, lanes, pf, pl); break;
+          case 1: acc = gather_sum<1>(a, rb, d, l, lanes, pf, pl); break;
           default: break;
         }
       }
@@ -462,11 +425,8 @@ PrLayout* pr_layout(gbg_graph* g) {
   if (!g->pr) {
     const uint64_t* voff = virtual_offsets(g);
     with_view(g, [&](auto view) { g->pr = build_layout(g, view, voff); });
-    g->pr->hot = static_cast<uint32_t>(std::min<uint64_t>(g->n, kHotMax));
-    const size_t smem = g->pr->hot * sizeof(double);
-    GBG_CUDA(cudaFuncSetAttribute(pr_iter_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 1;
-    GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pr_iter_k, kPrThreads, smem));
+    GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pr_iter_k, kPrThreads, 0));
     g->pr->grid = static_cast<uint32_t>(std::max(per_sm, 1) * g->sm_count);
     g->pr->blk = dalloc<double>(2 * g->pr->grid);
   }
@@ -504,8 +464,7 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
     a.nd = static_cast<double>(n);
     a.tol = tol;
     a.iter = static_cast<int>(it);
-    a.hot = L->hot;
-    GBG_LAUNCH(g, pr_iter_k, L->grid, kPrThreads, L->hot * sizeof(double), a);
+    GBG_LAUNCH(g, pr_iter_k, L->grid, kPrThreads, 0, a);
   }
   PrScalars hs;
   GBG_CUDA(cudaMemcpyAsync(g->hscalar, sc, sizeof(PrScalars), cudaMemcpyDeviceToHost, g->stream));
