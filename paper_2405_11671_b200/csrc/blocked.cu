@@ -430,7 +430,8 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
     g->m -= A;
   }
   g->invalidate_derived();
-  g->symmetric = false;  // arbitrary batches need not keep arc pairs
+  g->symmetric = false;  // arbitrary batches need not keep arc pairs: re-verify lazily
+  g->sym_checked = false;
   return A;
 }
 

@@ -141,7 +141,8 @@ struct gbg_graph {
   std::mutex mu;
   uint64_t launches = 0;
   int sm_count = 148;
-  bool symmetric = false;  // every arc's reverse present (set by the R-MAT builder)
+  bool symmetric = false;    // every arc's reverse present (set by the R-MAT builder)
+  bool sym_checked = false;  // symmetry verified on the device (cc.cu)
 
   // CSR storage
   uint64_t* off = nullptr;

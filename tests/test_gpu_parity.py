@@ -189,6 +189,7 @@ def test_scale24_bfs_cc_match_golden(gbg):
     assert digest(r.depth) == gd["bfs"]["digest"]
     assert r.modes == gd["bfs"]["modes"] and r.frontier_sizes == gd["bfs"]["frontier_sizes"]
     assert digest(gbg.cc(g)) == gd["cc"]["digest"]
+    assert gbg.triangle_count(g) == gd["tc"]["triangles"]
     p = gbg.pagerank(g, 0.85, 20, TINY)
     ids = np.array(gd["pagerank"]["sample_ids"])
     want = np.array([float.fromhex(h) for h in gd["pagerank"]["sample_hex"]])
@@ -255,6 +256,19 @@ def test_cc_matches_oracle(gbg, ref, orc, kind):
         n, pairs = ref.er(200 + 53 * trial, 0.008, 900 + trial)
         off, nbr = csr(n, pairs)
         assert np.array_equal(gbg.cc(mk(n, pairs)), orc.cc(n, off, nbr))
+
+
+def test_cc_asymmetric_arcs(gbg, orc):
+    """Directed arc sets (no reverse arcs): the full-hooking path, labels
+    still the minimum id of each weakly connected component."""
+    rng = np.random.default_rng(11)
+    for trial in range(10):
+        n = 300 + 100 * trial
+        raw = rng.integers(0, n, size=(n // 2, 2)).astype(np.uint32)
+        pairs = orc.prepare_global(raw)
+        off, nbr = csr(n, pairs)
+        for g in (gbg.CsrGraph.build(n, pairs), gbg.BlockedGraph.build(n, pairs)):
+            assert np.array_equal(gbg.cc(g), orc.cc(n, off, nbr)), trial
 
 
 def test_tc_known_answers(gbg, ref, orc):
