@@ -32,6 +32,7 @@
 #include <memory>
 #include <vector>
 
+#include "edges.cuh"
 #include "keys.cuh"
 
 namespace gbg {
@@ -171,29 +172,34 @@ __global__ void contains_k(G g, const uint32_t* pairs, uint64_t count, uint8_t* 
   }
 }
 
-// presence of each prepared arc in the container; keep those that change it
-struct ApplyIn {
-  const uint64_t* k;
-  BatchKeys bk;
-  const uint64_t* start;
-  const uint32_t* deg;
-  const uint32_t* pool;
-  int insert;
-  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+// presence of each prepared arc in the container (flag = changes the
+// container: absent for insert, present for delete) and its rank among the
+// source's current neighbours (the merge slot offset of an inserted arc)
+__global__ void apply_flags_k(const uint64_t* k, uint64_t U, BatchKeys bk, const uint64_t* start, const uint32_t* deg,
+                              const uint32_t* pool, int insert, uint32_t* flag, uint32_t* lb) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < U; i += stride) {
     const uint64_t x = k[i];
     const uint32_t s = bk.src(x), d = bk.dst(x);
     const uint32_t* lst = pool + start[s];
     const uint32_t len = deg[s];
     const uint32_t pos = lower_bound_u32(lst, len, d);
     const bool present = pos < len && lst[pos] == d;
-    return insert ? !present : present;
+    flag[i] = insert ? !present : present;
+    lb[i] = pos;
   }
-};
+}
 struct ApplyOut {
-  ApplyIn in;
+  const uint32_t* flag;
+  const uint64_t* k;
+  const uint32_t* lb;
   uint64_t* out;
+  uint32_t* out_lb;
   __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
-    if (in(i)) out[pre] = in.k[i];
+    if (flag[i]) {
+      out[pre] = k[i];
+      out_lb[pre] = lb[i];
+    }
   }
 };
 
@@ -249,71 +255,59 @@ struct OldDegIn {
   __device__ __forceinline__ uint64_t operator()(uint64_t gi) const { return deg[gsrc[gi]]; }
 };
 
-// expand flat index -> group via binary search over an exclusive scan
-__device__ __forceinline__ uint32_t find_group(const uint64_t* scan, uint32_t ng, uint64_t e) {
-  uint32_t lo = 0, hi = ng;  // scan[lo] <= e < scan[hi] (scan[ng] = total)
-  while (hi - lo > 1) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (scan[mid] <= e) lo = mid; else hi = mid;
+// Staging, merge and set difference run on the balanced segmented
+// expansion (edges.cuh: expand) over the touched groups.
+struct StageOp {  // segments = touched lists, sized by their old degree
+  const uint32_t* gsrc;
+  const uint64_t* start;
+  const uint32_t* pool;
+  uint32_t* staged;
+  __device__ __forceinline__ void operator()(uint32_t gi, uint32_t j, uint64_t e) const {
+    staged[e] = pool[start[gsrc[gi]] + j];
   }
-  return lo;
-}
+};
 
-__global__ void stage_old_k(uint32_t ng, const uint64_t* oscan, uint64_t total, const uint32_t* gsrc,
-                            const uint64_t* start, const uint32_t* pool, uint32_t* staged) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint32_t gi = find_group(oscan, ng, e);
-    staged[e] = pool[start[gsrc[gi]] + (e - oscan[gi])];
-  }
-}
-
-// old elements -> their slot in the new list
-__global__ void merge_old_k(uint32_t ng, const uint64_t* oscan, uint64_t total, const uint32_t* gsrc,
-                            const uint32_t* gstart, const uint32_t* gcnt, const uint64_t* akeys, BatchKeys bk,
-                            const uint32_t* staged, const uint64_t* newstart, uint32_t* pool, int insert) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint32_t gi = find_group(oscan, ng, e);
-    const uint32_t j = static_cast<uint32_t>(e - oscan[gi]);
+// old element j of group gi -> its slot in the new list: j plus (insert)
+// or minus (delete) its rank among the group's applied arcs
+struct MergeOldOp {
+  const uint32_t* gsrc;
+  const uint32_t* gstart;
+  const uint64_t* akeys;
+  BatchKeys bk;
+  const uint32_t* staged;
+  const uint64_t* newstart;
+  uint32_t* pool;
+  int insert;
+  __device__ __forceinline__ void operator()(uint32_t gi, uint32_t j, uint64_t e) const {
     const uint32_t x = staged[e];
-    // rank of x among the group's batch destinations
     const uint64_t* b = akeys + gstart[gi];
-    uint32_t lo = 0, hi = gcnt[gi];
+    const uint32_t cnt = gstart[gi + 1] - gstart[gi];
+    uint32_t lo = 0, hi = cnt;
     while (lo < hi) {
-      uint32_t mid = (lo + hi) >> 1;
+      const uint32_t mid = (lo + hi) >> 1;
       if (bk.dst(b[mid]) < x) lo = mid + 1; else hi = mid;
     }
     uint32_t* out = pool + newstart[gsrc[gi]];
     if (insert) {
       out[j + lo] = x;
-    } else {
-      const bool removed = lo < gcnt[gi] && bk.dst(b[lo]) == x;
-      if (!removed) out[j - lo] = x;
+    } else if (!(lo < cnt && bk.dst(b[lo]) == x)) {
+      out[j - lo] = x;
     }
   }
-}
+};
 
-// new elements (insert only) -> their slot
-__global__ void merge_new_k(uint32_t ng, uint32_t A, const uint32_t* gstart, const uint32_t* gsrc,
-                            const uint64_t* akeys, BatchKeys bk, const uint64_t* oscan, const uint32_t* staged,
-                            const uint64_t* newstart, uint32_t* pool) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < A; i += stride) {
-    // group of arc i: last head <= i
-    uint32_t lo = 0, hi = ng;
-    while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
-      if (gstart[mid] <= i) lo = mid; else hi = mid;
-    }
-    const uint32_t gi = lo;
-    const uint32_t r = static_cast<uint32_t>(i - gstart[gi]);
-    const uint32_t x = bk.dst(akeys[i]);
-    const uint32_t* old = staged + oscan[gi];
-    const uint32_t olen = static_cast<uint32_t>(oscan[gi + 1] - oscan[gi]);
-    pool[newstart[gsrc[gi]] + r + lower_bound_u32(old, olen, x)] = x;
+// inserted arc r of group gi -> slot r + (old neighbours below it)
+struct MergeNewOp {
+  const uint32_t* gsrc;
+  const uint64_t* akeys;
+  const uint32_t* alb;
+  BatchKeys bk;
+  const uint64_t* newstart;
+  uint32_t* pool;
+  __device__ __forceinline__ void operator()(uint32_t gi, uint32_t r, uint64_t i) const {
+    pool[newstart[gsrc[gi]] + r + alb[i]] = bk.dst(akeys[i]);
   }
-}
+};
 
 // destination of each touched list: in place, or a fresh bump allocation
 __global__ void plan_dest_k(uint32_t ng, const uint32_t* gsrc, const uint64_t* galloc_scan, const uint64_t* galloc,
@@ -369,8 +363,12 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   if (U == 0) return 0;
   uint32_t* cnt = g->ws.get<uint32_t>("upd.cnt", 4);
   uint64_t* akeys = g->ws.get<uint64_t>("upd.sorted", count);  // sorted buffer is free now
-  ApplyIn ain{ukeys, bk, g->bstart, g->bdeg, g->pool, insert ? 1 : 0};
-  device_scan<uint32_t>(g, ain, ApplyOut{ain, akeys}, U, cnt + 1, "upd.apply");
+  uint32_t* flag = g->ws.get<uint32_t>("upd.flag", U);
+  uint32_t* lb = g->ws.get<uint32_t>("upd.lb", U);
+  uint32_t* alb = g->ws.get<uint32_t>("upd.alb", U);
+  GBG_LAUNCH(g, apply_flags_k, grid_for(U, 256, g->sm_count * 16), 256, 0, ukeys, U, bk, g->bstart, g->bdeg, g->pool,
+             insert ? 1 : 0, flag, lb);
+  device_scan<uint32_t>(g, ArrayIn<uint32_t>{flag}, ApplyOut{flag, ukeys, lb, akeys, alb}, U, cnt + 1, "upd.apply");
   uint32_t A = 0;
   read_scalars(g, cnt + 1, sizeof(A), &A);
   if (A == 0) return 0;
@@ -379,6 +377,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   device_scan<uint32_t>(g, HeadIn{akeys, bk}, HeadOut{akeys, bk, gstart, gsrc}, A, cnt + 2, "upd.heads");
   uint32_t ng = 0;
   read_scalars(g, cnt + 2, sizeof(ng), &ng);
+  GBG_CUDA(cudaMemcpyAsync(gstart + ng, &A, sizeof(A), cudaMemcpyHostToDevice, g->stream));  // gstart[ng] = A
   uint32_t* gcnt = g->ws.get<uint32_t>("upd.gcnt", ng);
   uint32_t* gnewdeg = g->ws.get<uint32_t>("upd.gnewdeg", ng);
   uint32_t* gnewcap = g->ws.get<uint32_t>("upd.gnewcap", ng);
@@ -407,18 +406,12 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint64_t otot = 0;
   read_scalars(g, oscan + ng, sizeof(otot), &otot);
   uint32_t* staged = g->ws.get<uint32_t>("upd.staged", otot);
-  if (otot)
-    GBG_LAUNCH(g, stage_old_k, grid_for(otot, 256, g->sm_count * 16), 256, 0, ng, oscan, otot, gsrc, g->bstart,
-               g->pool, staged);
+  expand(g, oscan, ng, otot, StageOp{gsrc, g->bstart, g->pool, staged});
   // destinations
   uint64_t* newstart = g->ws.get<uint64_t>("upd.newstart", g->n);
   GBG_LAUNCH(g, plan_dest_k, grid_for(ng, 256), 256, 0, ng, gsrc, gascan, galloc, g->pool_top, g->bstart, newstart);
-  if (otot)
-    GBG_LAUNCH(g, merge_old_k, grid_for(otot, 256, g->sm_count * 16), 256, 0, ng, oscan, otot, gsrc, gstart, gcnt,
-               akeys, bk, staged, newstart, g->pool, insert ? 1 : 0);
-  if (insert)
-    GBG_LAUNCH(g, merge_new_k, grid_for(A, 256, g->sm_count * 16), 256, 0, ng, A, gstart, gsrc, akeys, bk, oscan,
-               staged, newstart, g->pool);
+  expand(g, oscan, ng, otot, MergeOldOp{gsrc, gstart, akeys, bk, staged, newstart, g->pool, insert ? 1 : 0});
+  if (insert) expand(g, gstart, ng, A, MergeNewOp{gsrc, akeys, alb, bk, newstart, g->pool});
   GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,
              g->bcap);
   uint64_t need = 0;

@@ -85,26 +85,30 @@ __global__ void cc_sample_k(G g, uint32_t r, uint32_t* parent) {
   }
 }
 
-// most frequent root among a fixed sample of vertices (ties -> smaller root)
-__global__ void cc_dominant_k(const uint32_t* parent, uint64_t n, uint32_t* out) {
+// most frequent root among a fixed sample of 1024 vertices (ties -> smaller
+// root); one thread per sample counts its matches, then a block argmax
+__global__ void __launch_bounds__(1024) cc_dominant_k(const uint32_t* parent, uint64_t n, uint32_t* out) {
   constexpr int S = 1024;
   __shared__ uint32_t s[S];
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    const uint64_t v = (static_cast<uint64_t>(i) * 2654435761u) % n;
-    s[i] = parent[v];
-  }
+  __shared__ uint64_t s_best[32];
+  const int i = threadIdx.x;
+  s[i] = parent[(static_cast<uint64_t>(i) * 2654435761u) % n];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t best = s[0], best_cnt = 0;
-    for (int i = 0; i < S; ++i) {
-      uint32_t c = 0;
-      for (int j = 0; j < S; ++j) c += s[j] == s[i];
-      if (c > best_cnt || (c == best_cnt && s[i] < best)) {
-        best = s[i];
-        best_cnt = c;
-      }
-    }
-    *out = best;
+  uint32_t c = 0;
+  const uint32_t mine = s[i];
+  for (int j = 0; j < S; ++j) c += s[j] == mine;
+  // key: higher count first, then smaller root
+  uint64_t key = (static_cast<uint64_t>(c) << 32) | (0xffffffffu - mine);
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t other = __shfl_xor_sync(0xffffffffu, key, o);
+    key = other > key ? other : key;
+  }
+  if ((i & 31) == 0) s_best[i >> 5] = key;
+  __syncthreads();
+  if (i == 0) {
+    uint64_t best = 0;
+    for (int k = 0; k < 32; ++k) best = s_best[k] > best ? s_best[k] : best;
+    *out = 0xffffffffu - static_cast<uint32_t>(best);
   }
 }
 
@@ -195,7 +199,7 @@ void cc_run(gbg_graph* g, uint32_t* labels_dev) {
       GBG_LAUNCH(g, cc_sample_k<G>, grid_for(n, 256), 256, 0, view, r, parent);
     GBG_LAUNCH(g, cc_compress_k, grid_for(n, 256), 256, 0, n, parent, parent);
     uint32_t* dom = g->ws.get<uint32_t>("cc.dom", 4);
-    GBG_LAUNCH(g, cc_dominant_k, 1, 256, 0, parent, n, dom);
+    GBG_LAUNCH(g, cc_dominant_k, 1, 1024, 0, parent, n, dom);
     uint32_t* list = g->ws.get<uint32_t>("cc.list", n);
     OutsideIn<G> oin{view, parent, dom};
     device_scan<uint32_t>(g, oin, OutsideOut<G>{oin, list}, n, dom + 1, "cc.out");

@@ -62,6 +62,59 @@ __global__ void __launch_bounds__(kEdgeThreads) for_each_edge_k(G g, const uint6
   }
 }
 
+// Segmented expansion: op(seg, rank, flat) for every flat index in
+// [0, total), where `scan` is the exclusive prefix of the segment sizes
+// (scan[nseg] = total) and seg is the segment holding flat.  Same tiling as
+// for_each_edge: one search per thread, then a walk; empty segments are
+// skipped by re-searching.
+template <class T>
+__device__ __forceinline__ uint32_t seg_of(const T* scan, uint32_t nseg, uint64_t e, uint32_t lo) {
+  uint32_t hi = nseg;  // scan[lo] <= e < scan[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (static_cast<uint64_t>(scan[mid]) <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <class T, class Op>
+__global__ void __launch_bounds__(kEdgeThreads) expand_k(const T* __restrict__ scan, uint32_t nseg, uint64_t total,
+                                                          Op op) {
+  __shared__ uint32_t s_seg[kEdgeTile];
+  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kEdgeTile;
+  if (e0 >= total) return;
+  const uint32_t len = static_cast<uint32_t>(total - e0 < kEdgeTile ? total - e0 : kEdgeTile);
+  {
+    const uint32_t k0 = threadIdx.x * kEdgeIPT;
+    if (k0 < len) {
+      uint32_t s = seg_of(scan, nseg, e0 + k0, 0);
+      uint64_t next = scan[s + 1];
+#pragma unroll
+      for (int j = 0; j < kEdgeIPT; ++j) {
+        if (k0 + j >= len) break;
+        if (next <= e0 + k0 + j) {
+          s = seg_of(scan, nseg, e0 + k0 + j, s + 1);
+          next = scan[s + 1];
+        }
+        s_seg[k0 + j] = s;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < len; k += kEdgeThreads) {
+    const uint32_t s = s_seg[k];
+    const uint64_t e = e0 + k;
+    op(s, static_cast<uint32_t>(e - scan[s]), e);
+  }
+}
+
+template <class T, class Op>
+void expand(gbg_graph* g, const T* scan, uint32_t nseg, uint64_t total, Op op) {
+  if (total == 0 || nseg == 0) return;
+  const uint64_t tiles = (total + kEdgeTile - 1) / kEdgeTile;
+  GBG_LAUNCH(g, (expand_k<T, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, scan, nseg, total, op);
+}
+
 template <class G, class Op>
 void for_each_edge(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Op op) {
   if (m == 0) return;
