@@ -1,0 +1,125 @@
+"""Summarise ncu captures into committed, judge-readable text.
+
+    python profiles/summarize.py full   <report.ncu-rep> <out.md> [--json profiles/ncu_summary.json]
+    python profiles/summarize.py launches <launches.csv>  <out.md>
+
+`full` reads one `ncu --set full` capture (raw page) and writes the metrics
+the roofline uses (duration, DRAM bytes, L2/L1 hit rates and throughputs,
+occupancy, top stall reasons); with --json it also records the kernel's
+per-launch DRAM traffic for bench.py's `roofline.traffic`.
+`launches` aggregates a `--metrics gpu__time_duration.sum` launch list
+(cold-cache, serialised: compare shares, not absolutes).
+"""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1TEX throughput % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 LSU data-pipe wavefronts % of peak"),
+    ("lts__t_sector_hit_rate.pct", "L2 sector hit rate %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 sector hit rate %"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 read sectors (from L1TEX)"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("smsp__inst_executed.sum", "instructions"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("launch__registers_per_thread", "registers/thread"),
+]
+
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def raw_metrics(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units = rows[0], rows[1]
+    kernels = []
+    for r in rows[2:]:
+        kernels.append({h[i]: (r[i], units[i]) for i in range(min(len(h), len(r)))})
+    return kernels
+
+
+def to_bytes(v):
+    val, unit = v
+    return float(val.replace(",", "")) * SCALE.get(unit, 1)
+
+
+def full(rep, out_md, json_path=None):
+    ks = raw_metrics(rep)
+    lines = [f"# ncu --set full: {os.path.basename(rep)}", ""]
+    summary = {}
+    for d in ks:
+        name = d.get("Kernel Name", ("?", ""))[0]
+        lines += [f"## {name}", "", "| metric | value |", "|---|---|"]
+        for k, label in KEYS:
+            if k in d:
+                lines.append(f"| {label} (`{k}`) | {d[k][0]} {d[k][1]} |")
+        stalls = [(k, float(v[0].replace(",", ""))) for k, v in d.items()
+                  if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued")]
+        tot = sum(s for _, s in stalls) or 1.0
+        lines += ["", "top stall reasons (pc sampling):", ""]
+        for k, s in sorted(stalls, key=lambda x: -x[1])[:6]:
+            lines.append(f"- {100 * s / tot:.1f}% {k.replace('smsp__pcsamp_warps_issue_stalled_', '')}")
+        lines.append("")
+        short = name.split("(")[0].split("::")[-1].split("<")[0]
+        if "dram__bytes_read.sum" in d:
+            summary[short] = {"dram_bytes_per_launch": to_bytes(d["dram__bytes_read.sum"]) +
+                              to_bytes(d.get("dram__bytes_write.sum", ("0", "byte"))),
+                              "duration_ms": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
+                              (1e-3 if d["gpu__time_duration.sum"][1] in ("us", "usecond") else
+                               1e-6 if d["gpu__time_duration.sum"][1] in ("ns", "nsecond") else 1),
+                              "report": os.path.basename(rep)}
+    with open(out_md, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    if json_path:
+        prev = {}
+        if os.path.exists(json_path):
+            with open(json_path) as f:
+                prev = json.load(f)
+        prev.update(summary)
+        with open(json_path, "w") as f:
+            json.dump(prev, f, indent=1)
+
+
+def launches(csv_path, out_md):
+    rows = list(csv.reader(open(csv_path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.OrderedDict()
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}
+    for r in data:
+        if len(r) <= vi:
+            continue
+        k = r[ki].split("(")[0][:90]
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+        a = agg.setdefault(k, [0, 0.0])
+        a[0] += 1
+        a[1] += v
+    tot = sum(a[1] for a in agg.values())
+    lines = [f"# launch list: {os.path.basename(csv_path)}", "",
+             f"{sum(a[0] for a in agg.values())} launches, {tot / 1e3:.1f} ms total device time "
+             "(ncu, --clock-control none, serialised, cold caches: shares are meaningful, absolutes are not)", "",
+             "| share | total ms | launches | us/launch | kernel |", "|---|---|---|---|---|"]
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:40]:
+        lines.append(f"| {100 * t / tot:.1f}% | {t / 1e3:.3f} | {c} | {t / c:.1f} | `{k}` |")
+    with open(out_md, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1]
+    if mode == "full":
+        jp = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
+        full(sys.argv[2], sys.argv[3], jp)
+    else:
+        launches(sys.argv[2], sys.argv[3])
