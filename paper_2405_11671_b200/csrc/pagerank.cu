@@ -28,7 +28,6 @@
 // of its gathers, in flight at once).  Results are mapped back to original
 // ids at the end.
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -177,24 +176,7 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   L->nbr = dalloc<uint32_t>(m);
   GBG_LAUNCH(g, order_from_keys_k, grid_for(n, 256), 256, 0, sorted, n, L->ord, L->pos);
   device_scan<uint64_t>(g, SortedDegIn{sorted}, ArrayOut<uint64_t>{L->off}, n, L->off + n, "prl.scan");
-  {
-    // relabel into a scratch array, then sort every list by new id: the hot
-    // (low) ids come first, and lanes of a warp reading consecutive list
-    // entries then touch fewer cache lines (the heads of hub lists are
-    // nearly dense)
-    uint32_t* unsorted = g->ws.get<uint32_t>("prl.unsorted", m);
-    for_each_edge(g, view, voff, m, RelabelOp{voff, L->pos, L->off, unsorted});
-    size_t stemp = 0;
-    GBG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, stemp, unsorted, L->nbr, static_cast<int64_t>(m),
-                                                 static_cast<int64_t>(n), L->off, L->off + 1, g->stream));
-    void* st = g->ws.get("prl.segsort", stemp);
-    GBG_CUDA(cub::DeviceSegmentedSort::SortKeys(st, stemp, unsorted, L->nbr, static_cast<int64_t>(m),
-                                                 static_cast<int64_t>(n), L->off, L->off + 1, g->stream));
-    g->launches += 3;
-    GBG_CUDA(cudaStreamSynchronize(g->stream));
-    g->ws.release("prl.unsorted");
-    g->ws.release("prl.segsort");
-  }
+  for_each_edge(g, view, voff, m, RelabelOp{voff, L->pos, L->off, L->nbr});
   uint32_t* bnd = g->ws.get<uint32_t>("prl.bnd", kClasses);
   GBG_LAUNCH(g, class_bounds_k, 1, 32, 0, L->off, n, bnd);
   uint32_t hb[kClasses];
@@ -301,7 +283,7 @@ __device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint64
 
 // Persistent: CTA b owns work units b, b + grid, ... (static assignment, so
 // the err / dangling fold is deterministic).
-__global__ void __launch_bounds__(kPrThreads) pr_iter_k(PrArgs a) {
+__global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
   __shared__ double s_red[33];
   __shared__ int s_flag;
   if (a.sc->done) return;
