@@ -77,15 +77,35 @@ __global__ void __launch_bounds__(256) tc_count_k(uint64_t mo, const uint64_t* _
                                                   unsigned long long* total) {
   __shared__ unsigned long long s_red[33];
   unsigned long long cnt = 0;
+  const int lane = threadIdx.x & 31;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < mo; e += stride) {
-    const uint32_t u = osrc[e], v = onbr[e];
-    const uint64_t ub = ooff[u], vb = ooff[v];
-    const uint32_t du = static_cast<uint32_t>(ooff[u + 1] - ub), dv = static_cast<uint32_t>(ooff[v + 1] - vb);
-    const uint32_t* a = onbr + (du <= dv ? ub : vb);
-    const uint32_t* b = onbr + (du <= dv ? vb : ub);
-    const uint32_t la = du <= dv ? du : dv, lb = du <= dv ? dv : du;
-    for (uint32_t i = 0; i < la; ++i) cnt += bsearch_u32(b, lb, __ldg(a + i));
+  // one arc per lane; arcs whose shorter list exceeds 32 entries are then
+  // intersected by the whole warp (32 binary searches at a time)
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < mo; base += stride) {
+    const uint64_t e = base + threadIdx.x;
+    const uint32_t* a = onbr;
+    const uint32_t* b = onbr;
+    uint32_t la = 0, lb = 0;
+    if (e < mo) {
+      const uint32_t u = osrc[e], v = onbr[e];
+      const uint64_t ub = ooff[u], vb = ooff[v];
+      const uint32_t du = static_cast<uint32_t>(ooff[u + 1] - ub), dv = static_cast<uint32_t>(ooff[v + 1] - vb);
+      a = onbr + (du <= dv ? ub : vb);
+      b = onbr + (du <= dv ? vb : ub);
+      la = du <= dv ? du : dv;
+      lb = du <= dv ? dv : du;
+    }
+    if (la <= 32)
+      for (uint32_t i = 0; i < la; ++i) cnt += bsearch_u32(b, lb, __ldg(a + i));
+    uint32_t hard = __ballot_sync(0xffffffffu, la > 32);
+    while (hard) {
+      const int l = __ffs(hard) - 1;
+      hard &= hard - 1;
+      const uint32_t* aa = reinterpret_cast<const uint32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(a), l));
+      const uint32_t* bb = reinterpret_cast<const uint32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(b), l));
+      const uint32_t na = __shfl_sync(0xffffffffu, la, l), nb = __shfl_sync(0xffffffffu, lb, l);
+      for (uint32_t i = lane; i < na; i += 32) cnt += bsearch_u32(bb, nb, __ldg(aa + i));
+    }
   }
   cnt = block_sum(cnt, s_red);
   if (threadIdx.x == 0 && cnt) atomicAdd(total, cnt);
