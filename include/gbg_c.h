@@ -111,6 +111,13 @@ gbg_status gbg_blocked_from_csr(gbg_graph* csr, gbg_graph** out);
 gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, double c,
                            uint64_t seed, int kind, gbg_graph** out);
 gbg_status gbg_graph_destroy(gbg_graph* g);
+/* GBCSR1 binary graph files (io.cpp:75-114; README.md:134-138): magic
+ * "GBCSR1\0\0", n and m as little-endian uint64, n+1 uint64 offsets, m uint32
+ * neighbour ids.  load = load_binary_csr (validated like csr.cpp:14-18 and
+ * io.cpp:91-108, GBG_ERR_FORMAT otherwise) straight into a device container
+ * of `kind`; save = save_binary from any container (lists ascending). */
+gbg_status gbg_load_gbcsr1(const char* path, int kind, gbg_graph** out);
+gbg_status gbg_save_gbcsr1(gbg_graph* g, const char* path);
 
 /* ---- read API (graph_container.hpp:39-60, csr.hpp:19-33) ------------ */
 gbg_status gbg_kind(const gbg_graph* g, int* kind);

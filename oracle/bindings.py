@@ -190,6 +190,25 @@ class Ref:
         self._check(self.L.gbref_update_batch(log2_n, a, b, c, size, seed, ptr(out, _u32p)))
         return out
 
+    def load_binary(self, path):
+        """gb::load_binary_csr (io.cpp:87-110) -> (n, offsets, neighbors)."""
+        L = self.L
+        L.gbref_load_binary.restype = C.c_void_p
+        L.gbref_load_binary.argtypes = [C.c_char_p]
+        for f in ("gbref_csr_n", "gbref_csr_m"):
+            getattr(L, f).restype = C.c_uint64
+            getattr(L, f).argtypes = [C.c_void_p]
+        L.gbref_csr_arrays.argtypes = [C.c_void_p, _u64p, _u32p]
+        h = L.gbref_load_binary(os.fsencode(path))
+        if not h:
+            raise RefError(L.gbref_last_error().decode())
+        n, m = L.gbref_csr_n(h), L.gbref_csr_m(h)
+        off = np.empty(n + 1, dtype=np.uint64)
+        nbr = np.empty(max(m, 1), dtype=np.uint32)
+        L.gbref_csr_arrays(h, ptr(off, _u64p), ptr(nbr, _u32p))
+        L.gbref_csr_free(h)
+        return n, off, nbr[:m]
+
     def prepare_global(self, pairs):
         pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.uint32).reshape(-1, 2))
         out = np.empty_like(pairs)
@@ -220,6 +239,12 @@ class RefCsr:
         out = np.empty(self.n, dtype=np.int32)
         self.ref._check(self.ref.L.gbref_bfs(self.h, src, ptr(out, _i32p)))
         return out
+
+    def save_binary(self, path):
+        """gb::save_binary (io.cpp:75-85)."""
+        L = self.ref.L
+        L.gbref_save_binary.argtypes = [C.c_void_p, C.c_char_p]
+        self.ref._check(L.gbref_save_binary(self.h, os.fsencode(path)))
 
     def bfs_trace(self, src, cap=64):
         modes = np.zeros(cap, dtype=np.int32)

@@ -38,6 +38,7 @@
 #include "gb/csr.hpp"
 #include "gb/facade.hpp"
 #include "gb/generators.hpp"
+#include "gb/io.hpp"
 #include "gb/parallel.hpp"
 #include "gb/registry.hpp"
 #include "gb/rng.hpp"
@@ -185,6 +186,23 @@ void* gbref_csr_from_pairs(uint64_t n, const uint32_t* pairs, uint64_t count) {
 }
 
 void gbref_csr_free(void* h) { delete static_cast<CsrGraph*>(h); }
+
+// gb::save_binary / gb::load_binary_csr (io.cpp:75-110)
+int gbref_save_binary(void* csr, const char* path) {
+  return guard([&] { save_binary(*static_cast<CsrGraph*>(csr), path); });
+}
+void* gbref_load_binary(const char* path) {
+  void* out = nullptr;
+  guard([&] { out = new CsrGraph(load_binary_csr(path)); });
+  return out;
+}
+uint64_t gbref_csr_n(void* csr) { return static_cast<CsrGraph*>(csr)->num_vertices(); }
+uint64_t gbref_csr_m(void* csr) { return static_cast<CsrGraph*>(csr)->num_edges(); }
+void gbref_csr_arrays(void* csr, uint64_t* off, uint32_t* nbr) {
+  const CsrGraph& c = *static_cast<CsrGraph*>(csr);
+  std::memcpy(off, c.offsets().data(), c.offsets().size() * sizeof(uint64_t));
+  std::memcpy(nbr, c.neighbors().data(), c.neighbors().size() * sizeof(uint32_t));
+}
 
 // BFS depths as int32 (-1 unreached), the BASELINE narrowing of
 // gb::bfs(...).distances (UINT64_MAX -> -1).

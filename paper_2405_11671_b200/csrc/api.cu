@@ -4,6 +4,7 @@
 // gb::CsrGraph (csr.hpp:12-53, csr.cpp:9-25), VertexSubset conversions
 // (vertex_subset.cpp:8-45).
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -225,6 +226,63 @@ gbg_status gbg_csr_from_arcs(uint64_t n, const uint32_t* arcs, uint64_t m, gbg_g
 
 gbg_status gbg_graph_destroy(gbg_graph* g) {
   return guard([&] { delete g; });
+}
+
+// ---- GBCSR1 files (io.cpp:75-114) ---------------------------------------
+static const char kGbcsrMagic[8] = {'G', 'B', 'C', 'S', 'R', '1', '\0', '\0'};
+
+gbg_status gbg_load_gbcsr1(const char* path, int kind, gbg_graph** out) {
+  return guard([&] {
+    if (!path || !out) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    if (kind != GBG_KIND_CSR && kind != GBG_KIND_BLOCKED) fail(GBG_ERR_CONFIG, "unknown container kind");
+    *out = nullptr;
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "rb"), &std::fclose);
+    if (!f) fail(GBG_ERR_FORMAT, std::string("cannot open binary graph: ") + path);
+    char magic[8];
+    uint64_t nm[2];
+    if (std::fread(magic, 1, 8, f.get()) != 8 || std::memcmp(magic, kGbcsrMagic, 8) != 0)
+      fail(GBG_ERR_FORMAT, std::string("binary graph: bad magic: ") + path);
+    if (std::fread(nm, sizeof(uint64_t), 2, f.get()) != 2) fail(GBG_ERR_FORMAT, "binary graph: truncated header");
+    const uint64_t n = nm[0], m = nm[1];
+    uint64_t* off = nullptr;
+    uint32_t* nbr = nullptr;
+    GBG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&off), (n + 1) * sizeof(uint64_t)));
+    std::unique_ptr<uint64_t, cudaError_t (*)(void*)> hold_off(off, &cudaFreeHost);
+    GBG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&nbr), (m ? m : 1) * sizeof(uint32_t)));
+    std::unique_ptr<uint32_t, cudaError_t (*)(void*)> hold_nbr(nbr, &cudaFreeHost);
+    if (std::fread(off, sizeof(uint64_t), n + 1, f.get()) != n + 1) fail(GBG_ERR_FORMAT, "binary graph: truncated offsets");
+    if (m && std::fread(nbr, sizeof(uint32_t), m, f.get()) != m) fail(GBG_ERR_FORMAT, "binary graph: truncated neighbors");
+    gbg_graph* csr = nullptr;
+    gbg_status st = gbg_csr_create(n, m, off, nbr, &csr);  // validates on the device
+    if (st != GBG_OK) fail(st, gbg_last_error());
+    if (kind == GBG_KIND_CSR) {
+      *out = csr;
+      return;
+    }
+    std::unique_ptr<gbg_graph> hold_csr(csr);
+    gbg_graph* b = nullptr;
+    st = gbg_blocked_from_csr(csr, &b);
+    if (st != GBG_OK) fail(st, gbg_last_error());
+    *out = b;
+  });
+}
+
+gbg_status gbg_save_gbcsr1(gbg_graph* g, const char* path) {
+  return guard([&] {
+    if (!g || !path) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    const uint64_t n = g->n, m = g->m;
+    std::vector<uint64_t> off(n + 1);
+    std::vector<uint32_t> nbr(m ? m : 1);
+    gbg_status st = gbg_export_csr(g, off.data(), nbr.data());
+    if (st != GBG_OK) fail(st, gbg_last_error());
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "wb"), &std::fclose);
+    if (!f) fail(GBG_ERR_FORMAT, std::string("cannot write binary graph: ") + path);
+    const uint64_t nm[2] = {n, m};
+    bool ok = std::fwrite(kGbcsrMagic, 1, 8, f.get()) == 8 && std::fwrite(nm, sizeof(uint64_t), 2, f.get()) == 2 &&
+              std::fwrite(off.data(), sizeof(uint64_t), n + 1, f.get()) == n + 1 &&
+              (m == 0 || std::fwrite(nbr.data(), sizeof(uint32_t), m, f.get()) == m);
+    if (!ok) fail(GBG_ERR_FORMAT, std::string("write failed: ") + path);
+  });
 }
 
 gbg_status gbg_kind(const gbg_graph* g, int* kind) {

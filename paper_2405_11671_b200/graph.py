@@ -151,6 +151,8 @@ _SIGS = {
     "gbg_update_batch_device": [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _vp],
     "gbg_contains_device": [_vp, _vp, C.c_uint64, _vp],
     "gbg_pagerank_prepare": [_vp, _f64p],
+    "gbg_load_gbcsr1": [C.c_char_p, C.c_int, _gpp],
+    "gbg_save_gbcsr1": [_vp, C.c_char_p],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_L, _name)
@@ -340,6 +342,18 @@ def generate_rmat(log2_n: int, arcs: int, seed: int, a=0.5, b=0.1, c=0.1, kind: 
     h = C.c_void_p()
     _check(_L.gbg_rmat_create(log2_n, arcs, a, b, c, seed, kind, C.byref(h)))
     return (CsrGraph if kind == KIND_CSR else BlockedGraph)(h.value)
+
+
+def load_binary(path: str, kind: int = KIND_CSR):
+    """gb::load_binary_csr (io.cpp:87-110): a GBCSR1 file into a device container."""
+    h = C.c_void_p()
+    _check(_L.gbg_load_gbcsr1(os.fsencode(path), kind, C.byref(h)))
+    return (CsrGraph if kind == KIND_CSR else BlockedGraph)(h.value)
+
+
+def save_binary(g: _Graph, path: str):
+    """gb::save_binary (io.cpp:75-85) from a device container."""
+    _check(_L.gbg_save_gbcsr1(g.handle, os.fsencode(path)))
 
 
 def generate_update_batch_device(log2_n: int, size: int, seed: int, out_ptr: int, a=0.5, b=0.1, c=0.1):

@@ -72,6 +72,38 @@ def test_static_csr_rejects_updates(gbg):
             f()
 
 
+def test_gbcsr1_files_interchange_with_reference(gbg, ref, tmp_path):
+    """GBCSR1 (io.cpp:75-114): files written by the reference load on the
+    device, and files written from the device are byte-identical to the
+    reference's and load back in it."""
+    n, pairs = ref.rmat(14, 16 << 14, 3)
+    off, nbr = csr(n, pairs)
+    ref_file = tmp_path / "ref.gbcsr"
+    ref.csr(n, off, nbr).save_binary(str(ref_file))
+    for kind in (gbg.KIND_CSR, gbg.KIND_BLOCKED):
+        g = gbg.load_binary(str(ref_file), kind)
+        go, gn = g.to_csr()
+        assert np.array_equal(go, off) and np.array_equal(gn, nbr)
+        ours = tmp_path / f"ours{kind}.gbcsr"
+        gbg.save_binary(g, str(ours))
+        assert ours.read_bytes() == ref_file.read_bytes()
+        rn, ro, rb = ref.load_binary(str(ours))
+        assert rn == n and np.array_equal(ro, off) and np.array_equal(rb, nbr)
+    bad = tmp_path / "bad.gbcsr"
+    bad.write_bytes(b"NOTCSR00" + ref_file.read_bytes()[8:])
+    with pytest.raises(gbg.FormatError):
+        gbg.load_binary(str(bad))
+    bad.write_bytes(ref_file.read_bytes()[:100])
+    with pytest.raises(gbg.FormatError):
+        gbg.load_binary(str(bad))
+    raw = bytearray(ref_file.read_bytes())
+    hdr = 8 + 16 + 8 * (n + 1)
+    raw[hdr:hdr + 8] = raw[hdr + 4:hdr + 8] + raw[hdr:hdr + 4]  # swap two ids of vertex 0's list
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(gbg.FormatError):
+        gbg.load_binary(str(bad))
+
+
 # ---------------------------------------------------------------- edge_map
 def test_edge_map_known_answers(gbg):
     g = gbg.CsrGraph.build(4, T4_PAIRS)
