@@ -37,6 +37,10 @@ gbg_graph* new_handle(int kind, uint64_t n) {
     GBG_CUDA(cudaGetDevice(&g->device));
     GBG_CUDA(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, g->device));
     GBG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    GBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, g->device));
+    uint64_t keep = UINT64_MAX;  // keep freed blocks in the pool for reuse
+    GBG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     GBG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g->hscalar), 64));
   } catch (...) {
     delete g;
@@ -136,6 +140,8 @@ using namespace gbg;
 
 gbg_graph::~gbg_graph() {
   DeviceScope ds(device);
+  AllocStream as(stream);
+  ws.clear();
   dfree(off);
   dfree(nbr);
   dfree(bstart);
@@ -145,7 +151,10 @@ gbg_graph::~gbg_graph() {
   dfree(voff);
   invalidate_derived();
   if (hscalar) cudaFreeHost(hscalar);
-  if (stream) cudaStreamDestroy(stream);
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
 }
 
 extern "C" {
@@ -179,6 +188,7 @@ gbg_status gbg_csr_create(uint64_t n, uint64_t m, const uint64_t* offsets, const
     *out = nullptr;
     gbg_graph* g = new_handle(GBG_KIND_CSR, n);
     std::unique_ptr<gbg_graph> hold(g);
+    AllocStream as(g->stream);
     g->m = m;
     g->off = dalloc<uint64_t>(n + 1);
     g->nbr = dalloc<uint32_t>(m);
@@ -204,6 +214,7 @@ gbg_status gbg_csr_from_arcs(uint64_t n, const uint32_t* arcs, uint64_t m, gbg_g
     *out = nullptr;
     gbg_graph* g = new_handle(GBG_KIND_CSR, n);
     std::unique_ptr<gbg_graph> hold(g);
+    AllocStream as(g->stream);
     g->m = m;
     g->off = dalloc<uint64_t>(n + 1);
     g->nbr = dalloc<uint32_t>(m);
@@ -416,6 +427,7 @@ gbg_status gbg_subset_to_dense(uint64_t n, const uint32_t* ids, uint64_t k, uint
     for (uint64_t i = 0; i < k; ++i)
       if (ids[i] >= n) fail(GBG_ERR_OUT_OF_RANGE, "VertexSubset: id out of range");
     std::unique_ptr<gbg_graph> g(new_handle(GBG_KIND_CSR, n));
+    AllocStream as(g->stream);
     uint64_t nw32 = (n + 31) / 32, nw64 = (n + 63) / 64;
     uint32_t* bm = g->ws.get<uint32_t>("bm", 2 * nw64);
     uint32_t* dids = g->ws.get<uint32_t>("ids", k);
@@ -438,6 +450,7 @@ gbg_status gbg_subset_to_sparse(uint64_t n, const uint64_t* words, uint32_t* ids
     if (n % 64 && nw64 && (words[nw64 - 1] >> (n % 64)))
       fail(GBG_ERR_OUT_OF_RANGE, "VertexSubset: bits at positions >= n must be zero");
     std::unique_ptr<gbg_graph> g(new_handle(GBG_KIND_CSR, n));
+    AllocStream as(g->stream);
     uint32_t* bm = g->ws.get<uint32_t>("bm", 2 * nw64);
     uint32_t* dids = g->ws.get<uint32_t>("ids", n);
     uint32_t* cnt = g->ws.get<uint32_t>("cnt", 1);

@@ -445,6 +445,7 @@ gbg_status gbg_blocked_create(uint64_t n, const uint32_t* arcs, uint64_t m, gbg_
     std::unique_ptr<gbg_graph> hold_csr(csr);
     gbg_graph* g = new_handle(GBG_KIND_BLOCKED, n);
     std::unique_ptr<gbg_graph> hold(g);
+    AllocStream as(g->stream);
     DeviceScope ds(g->device);
     g->m = m;
     GBG_CUDA(cudaStreamSynchronize(csr->stream));
@@ -463,6 +464,7 @@ gbg_status gbg_blocked_from_csr(gbg_graph* csr, gbg_graph** out) {
     GBG_CUDA(cudaStreamSynchronize(csr->stream));
     gbg_graph* g = new_handle(GBG_KIND_BLOCKED, csr->n);
     std::unique_ptr<gbg_graph> hold(g);
+    AllocStream as(g->stream);
     g->m = csr->m;
     blocked_from_device_csr(g, csr->n, csr->off, csr->nbr);
     GBG_CUDA(cudaStreamSynchronize(g->stream));

@@ -34,15 +34,30 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define GBG_CUDA(call) ::gbg::cuda_check((call), #call)
 
 // ---------------------------------------------------------------- memory
+// Device memory comes from the device's stream-ordered pool
+// (cudaMallocAsync) on the stream of the handle being worked on, so
+// building and dropping containers and scratch buffers never pays
+// cudaMalloc/cudaFree's device-wide synchronisation; the pool keeps freed
+// memory for reuse (release threshold raised in new_handle).
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+struct AllocStream {
+  cudaStream_t prev;
+  explicit AllocStream(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~AllocStream() { alloc_stream() = prev; }
+};
+
 template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  cuda_check(cudaMallocAsync(&p, count * sizeof(T), alloc_stream()), "cudaMallocAsync");
   return static_cast<T*>(p);
 }
 inline void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, alloc_stream());
 }
 
 // Named, growable device scratch buffers owned by a handle.  Buffers are
@@ -60,7 +75,7 @@ struct Workspace {
       b.p = nullptr;
       b.bytes = 0;
       size_t want = bytes + bytes / 8 + 256;
-      cuda_check(cudaMalloc(&b.p, want), "workspace cudaMalloc");
+      cuda_check(cudaMallocAsync(&b.p, want, alloc_stream()), "workspace cudaMallocAsync");
       b.bytes = want;
     }
     return b.p;
@@ -81,9 +96,11 @@ struct Workspace {
     for (auto& kv : bufs) t += kv.second.bytes;
     return t;
   }
-  ~Workspace() {
+  void clear() {
     for (auto& kv : bufs) dfree(kv.second.p);
+    bufs.clear();
   }
+  ~Workspace() { clear(); }
 };
 
 // ---------------------------------------------------------------- views
@@ -247,7 +264,8 @@ struct DeviceScope {
 #define GBG_HANDLE(g)                                                        \
   if (!(g)) ::gbg::fail(GBG_ERR_INVALID_ARGUMENT, "null graph handle");     \
   std::lock_guard<std::mutex> gbg_lock_((g)->mu);                            \
-  ::gbg::DeviceScope gbg_dev_((g)->device)
+  ::gbg::DeviceScope gbg_dev_((g)->device);                                  \
+  ::gbg::AllocStream gbg_as_((g)->stream)
 
 gbg_graph* new_handle(int kind, uint64_t n);
 void build_csr_offsets_from_sorted_src(gbg_graph* g, const uint32_t* src, uint64_t m, uint64_t* off);

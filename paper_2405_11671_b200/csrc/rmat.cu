@@ -106,6 +106,7 @@ gbg_status gbg_update_batch_device(uint32_t log2_n, double a, double b, double c
     if (!arcs_dev) fail(GBG_ERR_INVALID_ARGUMENT, "null output");
     RmatParams p = make_params(log2_n, a, b, c, seed);
     std::unique_ptr<gbg_graph> h(new_handle(GBG_KIND_CSR, 0));
+    AllocStream as(h->stream);
     GBG_LAUNCH(h.get(), rmat_batch_k, grid_for(size, 256, h->sm_count * 16), 256, 0, p, size, arcs_dev);
     GBG_CUDA(cudaStreamSynchronize(h->stream));
   });
@@ -120,6 +121,7 @@ gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, d
     RmatParams p = make_params(log2_n, a, b, c, seed);
     const uint64_t n = uint64_t{1} << log2_n;
     std::unique_ptr<gbg_graph> g(new_handle(GBG_KIND_CSR, n));
+    AllocStream as(g->stream);
     const BatchKeys bk{static_cast<int>(log2_n)};
     const uint64_t count = 2 * arcs;
     uint64_t m = 0;
@@ -148,6 +150,7 @@ gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, d
     g->ws.release("rmat.uniq.sums");
     if (kind == GBG_KIND_BLOCKED) {
       std::unique_ptr<gbg_graph> b(new_handle(GBG_KIND_BLOCKED, n));
+      AllocStream bas(b->stream);
       b->m = m;
       b->symmetric = true;
       blocked_from_device_csr(b.get(), n, g->off, g->nbr);
