@@ -5,8 +5,11 @@
 //   dense iff |F| + sum deg(F) > (1/20) * m        (traversal.cpp:105-106)
 // and the frontier representations follow the reference; the work inside
 // each level runs in the push_k / pull_k engines (traverse.cuh).  The host
-// reads back two scalars per level (|next| and sum deg(next)) to make the
-// same decision the reference makes.
+// reads back one packed scalar per level (|next| and sum deg(next)) to make
+// the same decision the reference makes.  A push level emits the next
+// frontier as an id list together with its degree prefix and bitmap, so the
+// following level starts without a scan or conversion; only a dense ->
+// sparse transition compacts a bitmap (one ordered scan).
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -55,23 +58,27 @@ struct MaskOp {
   __device__ __forceinline__ void dense_word(uint64_t, uint32_t) const {}
 };
 
-__global__ void bfs_init_k(uint32_t src, uint32_t* visited, int32_t* depth, uint32_t* list) {
-  visited[src >> 5] |= 1u << (src & 31);
+template <class G>
+__global__ void bfs_init_k(G g, uint32_t src, uint32_t* visited, int32_t* depth, uint32_t* list, uint64_t* dscan,
+                           uint32_t* bm, unsigned long long* packed) {
+  const uint32_t bit = 1u << (src & 31);
+  visited[src >> 5] |= bit;
+  bm[src >> 5] |= bit;
   depth[src] = 0;
   list[0] = src;
-}
-
-template <class G>
-__global__ void degree_of_k(G g, uint32_t v, unsigned long long* out) {
-  out[0] = 1;
-  out[1] = g.degree(v);
+  const uint32_t d = g.degree(src);
+  dscan[0] = 0;
+  dscan[1] = d;
+  *packed = (1ull << kPackShift) | d;
 }
 
 namespace {
 
-// Frontier state shared by BFS and edge_map: a list, a bitmap, or both.
+// One frontier: storage for all three representations, flags for which are
+// current.
 struct Frontier {
   uint32_t* list = nullptr;
+  uint64_t* dscan = nullptr;
   uint32_t* bm = nullptr;
   bool has_list = false, has_bm = false;
   uint64_t size = 0, degsum = 0;
@@ -79,19 +86,17 @@ struct Frontier {
 
 struct TraversalBuffers {
   uint64_t nw;  // 32-bit words
-  uint32_t *fb, *nb, *la, *lb;
-  uint64_t* dscan;
-  unsigned long long* counters;
-  uint32_t* cnt32;
+  Frontier a, b;
+  unsigned long long* packed;
   TraversalBuffers(gbg_graph* g) {
     nw = (g->n + 31) / 32;
-    fb = g->ws.get<uint32_t>("t.fb", nw + 2);
-    nb = g->ws.get<uint32_t>("t.nb", nw + 2);
-    la = g->ws.get<uint32_t>("t.la", g->n + 1);
-    lb = g->ws.get<uint32_t>("t.lb", g->n + 1);
-    dscan = g->ws.get<uint64_t>("t.dscan", g->n + 2);
-    counters = g->ws.get<unsigned long long>("t.counters", 4);
-    cnt32 = g->ws.get<uint32_t>("t.cnt32", 2);
+    a.bm = g->ws.get<uint32_t>("t.fa", nw + 2);
+    b.bm = g->ws.get<uint32_t>("t.fb", nw + 2);
+    a.list = g->ws.get<uint32_t>("t.la", g->n + 1);
+    b.list = g->ws.get<uint32_t>("t.lb", g->n + 1);
+    a.dscan = g->ws.get<uint64_t>("t.da", g->n + 2);
+    b.dscan = g->ws.get<uint64_t>("t.db", g->n + 2);
+    packed = g->ws.get<unsigned long long>("t.packed", 2);
   }
 };
 
@@ -104,47 +109,51 @@ unsigned pull_grid(gbg_graph* g, uint64_t nw) {
   return grid_for(nw * 32, kPullThreads, static_cast<unsigned>(g->sm_count) * 8u);
 }
 
-// One edge_map step.  `cur` is consumed (converted as needed); the output
-// frontier is written into `out` (list for sparse, bitmap for dense).
+void read_packed(gbg_graph* g, unsigned long long* packed, Frontier& f) {
+  unsigned long long p = 0;
+  read_scalars(g, packed, sizeof(p), &p);
+  f.size = pack_count(p);
+  f.degsum = pack_degsum(p);
+}
+
+// make the frontier's id list + degree prefix current (bitmap -> list)
+template <class G>
+void ensure_list(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& f) {
+  if (f.has_list) return;
+  device_scan<uint64_t>(g, PopcDegIn<G>{view, f.bm}, BitsToIdsDscanOut<G>{view, f.bm, f.list, f.dscan}, tb.nw,
+                        reinterpret_cast<uint64_t*>(tb.packed + 1), "b2l");
+  f.has_list = true;
+}
+
+// One edge_map step from `cur` into `out` (the other buffer set).
 template <class G, class Op, bool kEarly>
-void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, uint32_t* out_list,
-                   uint32_t* out_bm, bool dense, Op op, Frontier& out) {
-  GBG_CUDA(cudaMemsetAsync(tb.counters, 0, 2 * sizeof(unsigned long long), g->stream));
-  out = Frontier{};
+void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Frontier& out, bool dense, Op op) {
+  GBG_CUDA(cudaMemsetAsync(tb.packed, 0, sizeof(unsigned long long), g->stream));
+  out.has_list = out.has_bm = false;
   if (dense) {
     if (!cur.has_bm) {
       GBG_CUDA(cudaMemsetAsync(cur.bm, 0, tb.nw * sizeof(uint32_t), g->stream));
       if (cur.size) GBG_LAUNCH(g, list_to_bitmap_k, grid_for(cur.size, 256), 256, 0, cur.list, cur.size, cur.bm);
       cur.has_bm = true;
     }
-    GBG_CUDA(cudaMemsetAsync(out_bm, 0, tb.nw * sizeof(uint32_t), g->stream));
-    GBG_LAUNCH(g, (pull_k<G, Op, kEarly>), pull_grid(g, tb.nw), kPullThreads, 0, view, cur.bm, op, out_bm, tb.nw,
-               tb.counters);
-    out.bm = out_bm;
+    GBG_LAUNCH(g, (pull_k<G, Op, kEarly>), pull_grid(g, tb.nw), kPullThreads, 0, view, cur.bm, op, out.bm, tb.nw,
+               tb.packed);
     out.has_bm = true;
   } else {
-    if (!cur.has_list) {
-      GBG_CUDA(cudaMemsetAsync(tb.cnt32, 0, sizeof(uint32_t), g->stream));
-      bitmap_to_list(g, cur.bm, tb.nw, cur.list, tb.cnt32);
-      cur.has_list = true;
+    ensure_list(g, view, tb, cur);
+    GBG_CUDA(cudaMemsetAsync(out.bm, 0, tb.nw * sizeof(uint32_t), g->stream));
+    if (cur.size && cur.degsum) {
+      // sentinel dscan[|F|] = E closes the last segment for the binary searches
+      g->hscalar[4] = cur.degsum;
+      GBG_CUDA(cudaMemcpyAsync(cur.dscan + cur.size, g->hscalar + 4, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                               g->stream));
+      const uint64_t tiles = (cur.degsum + kPushTile - 1) / kPushTile;
+      GBG_LAUNCH(g, (push_k<G, Op>), static_cast<unsigned>(tiles), kPushThreads, 0, view, cur.list,
+                 static_cast<uint32_t>(cur.size), cur.dscan, cur.degsum, op, out.list, out.dscan, out.bm, tb.packed);
     }
-    if (cur.size) {
-      device_scan<uint64_t>(g, FrontierDegIn<G>{view, cur.list}, ArrayOut<uint64_t>{tb.dscan}, cur.size,
-                            tb.dscan + cur.size, "push.scan");
-      const uint64_t E = cur.degsum;
-      if (E) {
-        const uint64_t tiles = (E + kPushTile - 1) / kPushTile;
-        GBG_LAUNCH(g, (push_k<G, Op>), (unsigned)tiles, kPushThreads, 0, view, cur.list,
-                   static_cast<uint32_t>(cur.size), tb.dscan, E, op, out_list, tb.counters);
-      }
-    }
-    out.list = out_list;
-    out.has_list = true;
+    out.has_list = out.has_bm = true;
   }
-  unsigned long long c[2];
-  read_scalars(g, tb.counters, sizeof(c), c);
-  out.size = c[0];
-  out.degsum = c[1];
+  read_packed(g, tb.packed, out);
 }
 
 template <class G>
@@ -153,44 +162,27 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   uint32_t* visited = g->ws.get<uint32_t>("bfs.visited", tb.nw + 2);
   GBG_CUDA(cudaMemsetAsync(depth, 0xff, g->n * sizeof(int32_t), g->stream));
   GBG_CUDA(cudaMemsetAsync(visited, 0, tb.nw * sizeof(uint32_t), g->stream));
-  GBG_LAUNCH(g, bfs_init_k, 1, 1, 0, src, visited, depth, tb.la);
-  GBG_LAUNCH(g, degree_of_k<G>, 1, 1, 0, view, src, tb.counters);
-  unsigned long long c[2];
-  read_scalars(g, tb.counters, sizeof(c), c);
-  Frontier cur;
-  cur.list = tb.la;
-  cur.bm = tb.fb;
-  cur.has_list = true;
-  cur.size = 1;
-  cur.degsum = c[1];
-  uint32_t *spare_list = tb.lb, *spare_bm = tb.nb;
+  GBG_CUDA(cudaMemsetAsync(tb.a.bm, 0, tb.nw * sizeof(uint32_t), g->stream));
+  GBG_LAUNCH(g, bfs_init_k<G>, 1, 1, 0, view, src, visited, depth, tb.a.list, tb.a.dscan, tb.a.bm, tb.packed);
+  Frontier* cur = &tb.a;
+  Frontier* nxt = &tb.b;
+  read_packed(g, tb.packed, *cur);
+  cur->has_list = cur->has_bm = true;
   uint64_t reached = 1;
   int32_t level = 0;
   if (st) std::memset(st, 0, sizeof(*st));
-  while (cur.size > 0) {
+  while (cur->size > 0) {
     ++level;
-    const bool dense = choose_dense(cur.size, cur.degsum, g->m, 1.0 / 20.0);
+    const bool dense = choose_dense(cur->size, cur->degsum, g->m, 1.0 / 20.0);
     if (st && level - 1 < GBG_MAX_LEVELS) {
       st->mode[level - 1] = dense ? GBG_MODE_DENSE : GBG_MODE_SPARSE;
-      st->frontier[level - 1] = cur.size;
-      st->degree_sum[level - 1] = cur.degsum;
+      st->frontier[level - 1] = cur->size;
+      st->degree_sum[level - 1] = cur->degsum;
     }
-    Frontier nxt;
     BfsOp op{visited, depth, level};
-    edge_map_step<G, BfsOp, true>(g, view, tb, cur, spare_list, spare_bm, dense, op, nxt);
-    // recycle: the consumed frontier's storage becomes the spare
-    uint32_t* old_list = cur.list;
-    uint32_t* old_bm = cur.bm;
-    if (dense) {
-      nxt.list = old_list;  // storage for a later bitmap->list conversion
-      spare_bm = old_bm;
-      spare_list = spare_list;
-    } else {
-      nxt.bm = old_bm;
-      spare_list = old_list;
-    }
-    cur = nxt;
-    reached += cur.size;
+    edge_map_step<G, BfsOp, true>(g, view, tb, *cur, *nxt, dense, op);
+    std::swap(cur, nxt);
+    reached += cur->size;
   }
   if (st) {
     st->levels = static_cast<uint64_t>(level);
@@ -245,53 +237,32 @@ gbg_status gbg_edge_map(gbg_graph* g, const uint32_t* ids, uint64_t k, const uin
     GBG_CUDA(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), g->stream));
     // canonical VertexSubset (sorted, deduplicated; vertex_subset.cpp:8-15)
     // through the two conversion primitives
-    GBG_CUDA(cudaMemsetAsync(tb.fb, 0, tb.nw * sizeof(uint32_t), g->stream));
+    Frontier& cur = tb.a;
+    GBG_CUDA(cudaMemsetAsync(cur.bm, 0, tb.nw * sizeof(uint32_t), g->stream));
     if (k) {
       GBG_CUDA(cudaMemcpyAsync(raw, ids, k * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream));
-      GBG_LAUNCH(g, list_to_bitmap_k, grid_for(k, 256), 256, 0, raw, k, tb.fb);
+      GBG_LAUNCH(g, list_to_bitmap_k, grid_for(k, 256), 256, 0, raw, k, cur.bm);
     }
-    GBG_CUDA(cudaMemsetAsync(tb.cnt32, 0, sizeof(uint32_t), g->stream));
-    bitmap_to_list(g, tb.fb, tb.nw, tb.la, tb.cnt32);
-    uint32_t size = 0;
-    read_scalars(g, tb.cnt32, sizeof(size), &size);
-    Frontier cur;
-    cur.list = tb.la;
-    cur.bm = tb.fb;
-    cur.has_list = cur.has_bm = true;
-    cur.size = size;
+    cur.has_bm = true;
     with_view(g, [&](auto view) {
       using G = decltype(view);
-      // frontier work = |F| + sum deg(F) (traversal.hpp:15-20)
-      if (size) {
-        device_scan<uint64_t>(g, FrontierDegIn<G>{view, cur.list}, ArrayOut<uint64_t>{tb.dscan}, size,
-                              tb.dscan + size, "em.scan");
-        read_scalars(g, tb.dscan + size, sizeof(uint64_t), &cur.degsum);
-      }
+      // |F| and frontier work = |F| + sum deg(F) (traversal.hpp:15-20)
+      ensure_list(g, view, tb, cur);
+      read_packed(g, tb.packed + 1, cur);
       bool dense = mode == GBG_MODE_DENSE ||
                    (mode == GBG_MODE_AUTO && choose_dense(cur.size, cur.degsum, g->m, 1.0 / 20.0));
       if (mode_out) *mode_out = dense ? GBG_MODE_DENSE : GBG_MODE_SPARSE;
       MaskOp op{dcond, claimed, upd};
-      Frontier out;
+      Frontier& out = tb.b;
       if (dense && !early_exit)
-        edge_map_step<G, MaskOp, false>(g, view, tb, cur, tb.lb, tb.nb, true, op, out);
+        edge_map_step<G, MaskOp, false>(g, view, tb, cur, out, true, op);
       else
-        edge_map_step<G, MaskOp, true>(g, view, tb, cur, tb.lb, tb.nb, dense, op, out);
-      // membership bytes
-      std::vector<uint8_t> member(g->n, 0);
-      if (out.has_bm) {
-        std::vector<uint32_t> bm(tb.nw);
-        GBG_CUDA(cudaMemcpyAsync(bm.data(), out.bm, tb.nw * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
-        GBG_CUDA(cudaStreamSynchronize(g->stream));
-        for (uint64_t v = 0; v < g->n; ++v) member[v] = (bm[v >> 5] >> (v & 31)) & 1u;
-      } else {
-        std::vector<uint32_t> lst(out.size);
-        if (out.size)
-          GBG_CUDA(cudaMemcpyAsync(lst.data(), out.list, out.size * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                   g->stream));
-        GBG_CUDA(cudaStreamSynchronize(g->stream));
-        for (uint32_t v : lst) member[v] = 1;
-      }
-      std::memcpy(out_member, member.data(), g->n);
+        edge_map_step<G, MaskOp, true>(g, view, tb, cur, out, dense, op);
+      // membership bytes from the output bitmap (both modes produce one)
+      std::vector<uint32_t> bm(tb.nw);
+      GBG_CUDA(cudaMemcpyAsync(bm.data(), out.bm, tb.nw * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+      GBG_CUDA(cudaStreamSynchronize(g->stream));
+      for (uint64_t v = 0; v < g->n; ++v) out_member[v] = (bm[v >> 5] >> (v & 31)) & 1u;
     });
     unsigned long long hu = 0;
     read_scalars(g, upd, sizeof(hu), &hu);

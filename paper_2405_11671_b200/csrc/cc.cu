@@ -217,7 +217,7 @@ void cc_run(gbg_graph* g, uint32_t* labels_dev) {
         GBG_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), g->stream));
         const uint64_t tiles = (E + kPushTile - 1) / kPushTile;
         GBG_LAUNCH(g, (push_k<G, RestOp>), static_cast<unsigned>(tiles), kPushThreads, 0, view, list, k, dscan, E,
-                   RestOp{parent}, list, counters);
+                   RestOp{parent}, list, nullptr, nullptr, counters);
       }
     }
   });

@@ -53,6 +53,52 @@ inline void bitmap_to_list(gbg_graph* g, const uint32_t* bm, uint64_t nwords, ui
   device_scan<uint32_t>(g, PopcIn{bm}, BitsToIdsOut{bm, ids}, nwords, count_dev, "b2l");
 }
 
+// Frontier counters packed into one 64-bit word, (count << 36) | degree sum,
+// so a single atomic hands an emitting warp both its list slots and its
+// offsets in the next level's edge space: the push output is its own
+// exclusive degree prefix and the next sparse level needs no scan.
+constexpr int kPackShift = 36;
+constexpr uint64_t kPackMask = (uint64_t{1} << kPackShift) - 1;
+__host__ __device__ __forceinline__ uint64_t pack_count(uint64_t p) { return p >> kPackShift; }
+__host__ __device__ __forceinline__ uint64_t pack_degsum(uint64_t p) { return p & kPackMask; }
+
+// bitmap -> ascending id list plus the exclusive prefix of the members'
+// degrees (one scan over words of packed (popc, sum of degrees))
+template <class G>
+struct PopcDegIn {
+  G g;
+  const uint32_t* bm;
+  __device__ __forceinline__ uint64_t operator()(uint64_t w) const {
+    uint32_t bits = bm[w];
+    uint64_t d = 0;
+    const uint64_t c = __popc(bits);
+    while (bits) {
+      d += g.degree(static_cast<uint32_t>(w * 32 + __ffs(bits) - 1));
+      bits &= bits - 1;
+    }
+    return (c << kPackShift) | d;
+  }
+};
+template <class G>
+struct BitsToIdsDscanOut {
+  G g;
+  const uint32_t* bm;
+  uint32_t* ids;
+  uint64_t* dscan;
+  __device__ __forceinline__ void operator()(uint64_t w, uint64_t pre) const {
+    uint32_t bits = bm[w];
+    uint64_t c = pack_count(pre), d = pack_degsum(pre);
+    while (bits) {
+      const uint32_t v = static_cast<uint32_t>(w * 32 + __ffs(bits) - 1);
+      ids[c] = v;
+      dscan[c] = d;
+      d += g.degree(v);
+      ++c;
+      bits &= bits - 1;
+    }
+  }
+};
+
 // ---------------------------------------------------------------- push
 constexpr int kPushThreads = 256;
 constexpr int kPushIPT = 8;
@@ -69,11 +115,14 @@ struct FrontierDegIn {
 // [t*kPushTile, (t+1)*kPushTile) of the concatenated neighbour lists; the
 // owning frontier slot of each edge comes from a per-thread binary search
 // of the exclusive degree scan, then edges are walked with consecutive
-// threads on consecutive neighbours (coalesced within a list).
+// threads on consecutive neighbours (coalesced within a list).  Emitted
+// vertices are appended to `out` with their degree prefix in `out_dscan`
+// (packed counter, see pack_count) and set in the bitmap `out_bm`.
 template <class G, class Op>
 __global__ void __launch_bounds__(kPushThreads)
     push_k(G g, const uint32_t* __restrict__ F, uint32_t nf, const uint64_t* __restrict__ dscan,
-           uint64_t E, Op op, uint32_t* __restrict__ out, unsigned long long* counters) {
+           uint64_t E, Op op, uint32_t* __restrict__ out, uint64_t* __restrict__ out_dscan,
+           uint32_t* __restrict__ out_bm, unsigned long long* packed) {
   __shared__ uint32_t s_idx[kPushTile];
   const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kPushTile;
   if (e0 >= E) return;
@@ -99,7 +148,6 @@ __global__ void __launch_bounds__(kPushThreads)
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  unsigned long long emitted = 0, degsum = 0;
   for (uint32_t base = 0; base < len; base += kPushThreads) {
     const uint32_t k = base + threadIdx.x;
     bool emit = false;
@@ -115,19 +163,22 @@ __global__ void __launch_bounds__(kPushThreads)
     }
     const uint32_t mask = __ballot_sync(0xffffffffu, emit);
     if (mask) {
-      uint32_t pos = 0;
+      const uint64_t dv = emit ? g.degree(v) : 0;
+      const uint64_t dinc = warp_inclusive_scan(dv);
+      const uint64_t dtot = __shfl_sync(0xffffffffu, dinc, 31);
       const int leader = __ffs(mask) - 1;
-      if (lane == leader) pos = static_cast<uint32_t>(atomicAdd(counters, (unsigned long long)__popc(mask)));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
+      uint64_t old = 0;
+      if (lane == leader)
+        old = atomicAdd(packed, (static_cast<unsigned long long>(__popc(mask)) << kPackShift) | dtot);
+      old = __shfl_sync(0xffffffffu, old, leader);
       if (emit) {
-        out[pos + __popc(mask & ((1u << lane) - 1))] = v;
-        degsum += g.degree(v);
+        const uint64_t pos = pack_count(old) + __popc(mask & ((1u << lane) - 1));
+        out[pos] = v;
+        if (out_dscan) out_dscan[pos] = pack_degsum(old) + dinc - dv;
+        if (out_bm) atomicOr(out_bm + (v >> 5), 1u << (v & 31));
       }
-      emitted += __popc(mask);
     }
   }
-  degsum = warp_sum(degsum);
-  if (lane == 0 && degsum) atomicAdd(counters + 1, degsum);
 }
 
 // ---------------------------------------------------------------- pull
@@ -142,7 +193,7 @@ constexpr uint32_t kPullSerial = 8;  // neighbours a lane scans before the warp 
 template <class G, class Op, bool kEarly>
 __global__ void __launch_bounds__(kPullThreads)
     pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
-           unsigned long long* counters) {
+           unsigned long long* packed) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -195,20 +246,15 @@ __global__ void __launch_bounds__(kPullThreads)
       if (lane == l && fl) found = true;
     }
     const uint32_t fm = __ballot_sync(0xffffffffu, found);
+    if (lane == 0) nb[w] = fm;  // every word written: no clearing pass needed
     if (fm) {
-      if (lane == 0) {
-        nb[w] = fm;
-        op.dense_word(w, fm);
-      }
+      if (lane == 0) op.dense_word(w, fm);
       cnt += __popc(fm);
       if (found) degsum += d;
     }
   }
   degsum = warp_sum(degsum);
-  if (lane == 0 && cnt) {
-    atomicAdd(counters, cnt);
-    atomicAdd(counters + 1, degsum);
-  }
+  if (lane == 0 && cnt) atomicAdd(packed, (static_cast<unsigned long long>(cnt) << kPackShift) | degsum);
 }
 
 }  // namespace gbg
