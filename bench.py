@@ -419,6 +419,7 @@ def main():
         g500 = int(deg[d >= 0].sum() // 2)
         workloads[f"bfs_s{S}"] = {"ms": tb * 1e3, "gteps_graph500": g500 / tb / 1e9, "arcs_per_s": m / tb,
                                   "modes": st["modes"], "frontier_sizes": st["frontier_sizes"],
+                                  "level_ms": st["level_ms"],
                                   "reached": st["reached"], "source": src,
                                   "model_bytes_lower_bound": bfs_model_bytes(n, off, d, st["modes"],
                                                                              st["frontier_sizes"], st["degree_sums"])}

@@ -77,6 +77,7 @@ typedef struct gbg_bfs_stats {
   uint64_t frontier[GBG_MAX_LEVELS];     /* |F| fed to level i             */
   uint64_t degree_sum[GBG_MAX_LEVELS];   /* sum deg(F) fed to level i      */
   uint64_t reached;                      /* vertices with depth >= 0       */
+  float level_ms[GBG_MAX_LEVELS];        /* device time of level i (events) */
 } gbg_bfs_stats;
 
 /* ---- errors / runtime ---------------------------------------------- */

@@ -171,6 +171,13 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   uint64_t reached = 1;
   int32_t level = 0;
   if (st) std::memset(st, 0, sizeof(*st));
+  cudaEvent_t ev[GBG_MAX_LEVELS + 1];
+  int nev = 0;
+  if (st) {
+    GBG_CUDA(cudaEventCreate(&ev[0]));
+    GBG_CUDA(cudaEventRecord(ev[0], g->stream));
+    nev = 1;
+  }
   while (cur->size > 0) {
     ++level;
     const bool dense = choose_dense(cur->size, cur->degsum, g->m, 1.0 / 20.0);
@@ -181,8 +188,18 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
     }
     BfsOp op{visited, depth, level};
     edge_map_step<G, BfsOp, true>(g, view, tb, *cur, *nxt, dense, op);
+    if (st && nev <= GBG_MAX_LEVELS) {
+      GBG_CUDA(cudaEventCreate(&ev[nev]));
+      GBG_CUDA(cudaEventRecord(ev[nev], g->stream));
+      ++nev;
+    }
     std::swap(cur, nxt);
     reached += cur->size;
+  }
+  if (st) {
+    GBG_CUDA(cudaEventSynchronize(ev[nev - 1]));
+    for (int i = 1; i < nev; ++i) cudaEventElapsedTime(&st->level_ms[i - 1], ev[i - 1], ev[i]);
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
   }
   if (st) {
     st->levels = static_cast<uint64_t>(level);
