@@ -10,6 +10,8 @@
 // frontier as an id list together with its degree prefix and bitmap, so the
 // following level starts without a scan or conversion; only a dense ->
 // sparse transition compacts a bitmap (one ordered scan).
+#include <cooperative_groups.h>
+
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -70,6 +72,139 @@ __global__ void bfs_init_k(G g, uint32_t src, uint32_t* visited, int32_t* depth,
   dscan[0] = 0;
   dscan[1] = d;
   *packed = (1ull << kPackShift) | d;
+}
+
+// ---------------------------------------------------------------- persistent BFS
+// The whole level loop in one cooperative launch: every CTA evaluates the
+// same switch rule from the device-resident packed counter, runs its share
+// of the pull (grid-stride over bitmap words) or push (grid-stride over
+// edge tiles), and a grid-wide barrier separates levels.  This removes the
+// host round trip and the launch chain of each level.
+struct CoopState {
+  uint32_t* visited;
+  int32_t* depth;
+  uint32_t* list[2];
+  uint64_t* dscan[2];
+  uint32_t* bm[2];
+  unsigned long long* packed;  // ring of 3 level counters
+  uint64_t* level_packed;      // [GBG_MAX_LEVELS] per-level (count, degsum) of the input frontier
+  int32_t* level_mode;         // [GBG_MAX_LEVELS]
+  unsigned long long* level_ns;  // [GBG_MAX_LEVELS + 1] globaltimer at level boundaries
+  uint64_t* blocksum;          // [gridDim] conversion scan scratch
+  uint64_t* result;            // [0] levels, [1] reached
+  uint64_t nw;
+  double threshold;            // (1/20) * m, evaluated on the host like traversal.cpp:105-106
+  uint32_t src;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// grid-wide ordered compaction bitmap -> (ids, degree prefix); each CTA
+// owns a contiguous word range, each thread a contiguous sub-range
+template <class G>
+__device__ void coop_bitmap_to_list(cooperative_groups::grid_group& grid, G g, const uint32_t* bm, uint64_t nw,
+                                    uint32_t* ids, uint64_t* dscan, uint64_t* blocksum, uint64_t* s_red) {
+  const uint64_t per_cta = (nw + gridDim.x - 1) / gridDim.x;
+  const uint64_t w0 = blockIdx.x * per_cta;
+  const uint64_t w1 = w0 + per_cta < nw ? w0 + per_cta : nw;
+  const uint64_t per_thr = (per_cta + blockDim.x - 1) / blockDim.x;
+  const uint64_t t0 = w0 + threadIdx.x * per_thr;
+  const uint64_t t1 = t0 + per_thr < w1 ? t0 + per_thr : w1;
+  PopcDegIn<G> in{g, bm};
+  uint64_t local = 0;
+  for (uint64_t w = t0; w < t1; ++w) local += in(w);
+  const uint64_t btot = block_sum(local, s_red);
+  if (threadIdx.x == 0) blocksum[blockIdx.x] = btot;
+  grid.sync();
+  uint64_t pre = 0;
+  for (uint64_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) pre += blocksum[b];
+  pre = block_sum(pre, s_red);
+  uint64_t tot;
+  const uint64_t mine = block_exclusive_scan(local, s_red, tot) + pre;
+  BitsToIdsDscanOut<G> out{g, bm, ids, dscan};
+  uint64_t run = mine;
+  for (uint64_t w = t0; w < t1; ++w) {
+    out(w, run);
+    run += in(w);
+  }
+}
+
+template <class G>
+__global__ void __launch_bounds__(kPushThreads) bfs_coop_k(G g, CoopState s) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ uint32_t s_idx[kPushTile];
+  __shared__ uint64_t s_red[33];
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = tid; i < g.n; i += nthreads) s.depth[i] = -1;
+  for (uint64_t w = tid; w < s.nw; w += nthreads) {
+    s.visited[w] = 0;
+    s.bm[0][w] = 0;
+  }
+  if (tid < 3) s.packed[tid] = 0;
+  grid.sync();
+  if (tid == 0) {
+    const uint32_t bit = 1u << (s.src & 31);
+    s.visited[s.src >> 5] |= bit;
+    s.bm[0][s.src >> 5] |= bit;
+    s.depth[s.src] = 0;
+    s.list[0][0] = s.src;
+    const uint32_t d = g.degree(s.src);
+    s.dscan[0][0] = 0;
+    s.packed[0] = (1ull << kPackShift) | d;
+    s.level_ns[0] = globaltimer();
+  }
+  grid.sync();
+  int cur = 0;
+  bool has_list = true;
+  uint64_t reached = 1;
+  int32_t level = 1;
+  for (;; ++level) {
+    const unsigned long long p = *reinterpret_cast<volatile unsigned long long*>(s.packed + (level - 1) % 3);
+    const uint64_t size = pack_count(p), degsum = pack_degsum(p);
+    if (size == 0) break;
+    reached += level > 1 ? size : 0;
+    const bool dense = static_cast<double>(size + degsum) > s.threshold;
+    if (tid == 0) {
+      s.packed[(level + 1) % 3] = 0;  // last read at the start of level - 1
+      if (level <= GBG_MAX_LEVELS) {
+        s.level_packed[level - 1] = p;
+        s.level_mode[level - 1] = dense ? GBG_MODE_DENSE : GBG_MODE_SPARSE;
+      }
+    }
+    const int nxt = cur ^ 1;
+    BfsOp op{s.visited, s.depth, level};
+    unsigned long long* acc = s.packed + level % 3;
+    if (dense) {
+      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc);
+      has_list = false;
+    } else {
+      if (!has_list) {
+        coop_bitmap_to_list(grid, g, s.bm[cur], s.nw, s.list[cur], s.dscan[cur], s.blocksum, s_red);
+        has_list = true;
+      }
+      if (tid == 0) s.dscan[cur][size] = degsum;  // sentinel closing the last segment
+      for (uint64_t w = tid; w < s.nw; w += nthreads) s.bm[nxt][w] = 0;
+      grid.sync();
+      const uint64_t tiles = (degsum + kPushTile - 1) / kPushTile;
+      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        push_tile(g, s.list[cur], static_cast<uint32_t>(size), s.dscan[cur], degsum, op, s.list[nxt], s.dscan[nxt],
+                  s.bm[nxt], acc, t, s_idx);
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    if (tid == 0 && level <= GBG_MAX_LEVELS) s.level_ns[level] = globaltimer();
+    cur = nxt;
+  }
+  if (tid == 0) {
+    s.result[0] = static_cast<uint64_t>(level - 1);
+    s.result[1] = reached;
+  }
 }
 
 namespace {
@@ -156,8 +291,62 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
   read_packed(g, tb.packed, out);
 }
 
+// The persistent path; false when the device cannot co-schedule the grid.
+template <class G>
+bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* st) {
+  int coop = 0;
+  GBG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device));
+  int per_sm = 0;
+  GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_coop_k<G>, kPushThreads, 0));
+  if (!coop || per_sm < 1) return false;
+  const unsigned grid = static_cast<unsigned>(per_sm * g->sm_count);
+  TraversalBuffers tb(g);
+  CoopState s;
+  s.visited = g->ws.get<uint32_t>("bfs.visited", tb.nw + 2);
+  s.depth = depth;
+  s.list[0] = tb.a.list;
+  s.list[1] = tb.b.list;
+  s.dscan[0] = tb.a.dscan;
+  s.dscan[1] = tb.b.dscan;
+  s.bm[0] = tb.a.bm;
+  s.bm[1] = tb.b.bm;
+  s.packed = g->ws.get<unsigned long long>("bfs.ring", 4);
+  uint64_t* stat = g->ws.get<uint64_t>("bfs.stat", 3 * GBG_MAX_LEVELS + 8);
+  s.level_packed = stat;
+  s.level_ns = reinterpret_cast<unsigned long long*>(stat + GBG_MAX_LEVELS);
+  s.result = stat + 2 * GBG_MAX_LEVELS + 2;
+  s.level_mode = g->ws.get<int32_t>("bfs.modes", GBG_MAX_LEVELS);
+  s.blocksum = g->ws.get<uint64_t>("bfs.blocksum", grid);
+  s.nw = tb.nw;
+  s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
+  s.src = src;
+  void* args[] = {&view, &s};
+  GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
+                                       g->stream));
+  g->launches++;
+  std::vector<uint64_t> hs(3 * GBG_MAX_LEVELS + 8);
+  std::vector<int32_t> hm(GBG_MAX_LEVELS);
+  GBG_CUDA(cudaMemcpyAsync(hs.data(), stat, hs.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
+  GBG_CUDA(cudaMemcpyAsync(hm.data(), s.level_mode, hm.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+  GBG_CUDA(cudaStreamSynchronize(g->stream));
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    const uint64_t levels = hs[2 * GBG_MAX_LEVELS + 2];
+    st->levels = levels;
+    st->reached = hs[2 * GBG_MAX_LEVELS + 3];
+    for (uint64_t i = 0; i < levels && i < GBG_MAX_LEVELS; ++i) {
+      st->mode[i] = hm[i];
+      st->frontier[i] = pack_count(hs[i]);
+      st->degree_sum[i] = pack_degsum(hs[i]);
+      st->level_ms[i] = static_cast<float>((hs[GBG_MAX_LEVELS + i + 1] - hs[GBG_MAX_LEVELS + i]) * 1e-6);
+    }
+  }
+  return true;
+}
+
 template <class G>
 void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* st) {
+  if (bfs_coop(g, view, src, depth, st)) return;
   TraversalBuffers tb(g);
   uint32_t* visited = g->ws.get<uint32_t>("bfs.visited", tb.nw + 2);
   GBG_CUDA(cudaMemsetAsync(depth, 0xff, g->n * sizeof(int32_t), g->stream));

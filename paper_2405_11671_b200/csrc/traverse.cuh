@@ -118,13 +118,14 @@ struct FrontierDegIn {
 // threads on consecutive neighbours (coalesced within a list).  Emitted
 // vertices are appended to `out` with their degree prefix in `out_dscan`
 // (packed counter, see pack_count) and set in the bitmap `out_bm`.
+// Frontier data (list, prefix, bitmaps) may have been written earlier in
+// the same launch by the persistent BFS kernel, so it is read with plain
+// (coherent) loads; only the graph itself goes through the read-only path.
 template <class G, class Op>
-__global__ void __launch_bounds__(kPushThreads)
-    push_k(G g, const uint32_t* __restrict__ F, uint32_t nf, const uint64_t* __restrict__ dscan,
-           uint64_t E, Op op, uint32_t* __restrict__ out, uint64_t* __restrict__ out_dscan,
-           uint32_t* __restrict__ out_bm, unsigned long long* packed) {
-  __shared__ uint32_t s_idx[kPushTile];
-  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kPushTile;
+__device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, const uint64_t* dscan, uint64_t E,
+                                          Op op, uint32_t* out, uint64_t* out_dscan, uint32_t* out_bm,
+                                          unsigned long long* packed, uint64_t tile, uint32_t* s_idx) {
+  const uint64_t e0 = tile * kPushTile;
   if (e0 >= E) return;
   const uint32_t len = static_cast<uint32_t>(E - e0 < kPushTile ? E - e0 : kPushTile);
   {
@@ -154,11 +155,11 @@ __global__ void __launch_bounds__(kPushThreads)
     uint32_t v = 0;
     if (k < len) {
       const uint32_t i = s_idx[k];
-      const uint32_t u = __ldg(F + i);
+      const uint32_t u = F[i];
       uint64_t b;
       uint32_t d;
       g.seg(u, b, d);
-      v = g.at(b + (e0 + k - __ldg(dscan + i)));
+      v = g.at(b + (e0 + k - dscan[i]));
       emit = op.cond(v) && op.claim(v) && op.update(u, v);
     }
     const uint32_t mask = __ballot_sync(0xffffffffu, emit);
@@ -181,6 +182,15 @@ __global__ void __launch_bounds__(kPushThreads)
   }
 }
 
+template <class G, class Op>
+__global__ void __launch_bounds__(kPushThreads)
+    push_k(G g, const uint32_t* __restrict__ F, uint32_t nf, const uint64_t* __restrict__ dscan,
+           uint64_t E, Op op, uint32_t* __restrict__ out, uint64_t* __restrict__ out_dscan,
+           uint32_t* __restrict__ out_bm, unsigned long long* packed) {
+  __shared__ uint32_t s_idx[kPushTile];
+  push_tile(g, F, nf, dscan, E, op, out, out_dscan, out_bm, packed, blockIdx.x, s_idx);
+}
+
 // ---------------------------------------------------------------- pull
 constexpr int kPullThreads = 256;
 constexpr uint32_t kPullSerial = 8;  // neighbours a lane scans before the warp helps
@@ -190,10 +200,11 @@ constexpr uint32_t kPullSerial = 8;  // neighbours a lane scans before the warp 
 // vertex; vertices still unresolved with longer lists are then scanned by
 // the whole warp, 32 neighbours per step, ballot on frontier hits, stopping
 // at the first hit in list order when early exit applies.
+__device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
+
 template <class G, class Op, bool kEarly>
-__global__ void __launch_bounds__(kPullThreads)
-    pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
-           unsigned long long* packed) {
+__device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
+                                           unsigned long long* packed) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(kPullThreads)
       const uint32_t lim = d < kPullSerial ? d : kPullSerial;
       for (uint32_t j = 0; j < lim; ++j) {
         const uint32_t u = g.at(b + j);
-        if (bit_test(fb, u) && op.update(u, v)) {
+        if (frontier_bit(fb, u) && op.update(u, v)) {
           found = true;
           if (kEarly) break;
         }
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(kPullThreads)
       for (uint32_t j0 = kPullSerial; j0 < dd; j0 += 32) {
         const uint32_t j = j0 + lane;
         uint32_t u = 0;
-        const bool hit = j < dd && bit_test(fb, u = g.at(bb + j));
+        const bool hit = j < dd && frontier_bit(fb, u = g.at(bb + j));
         const uint32_t hm = __ballot_sync(0xffffffffu, hit);
         if (!hm) continue;
         if (kEarly) {
@@ -255,6 +266,13 @@ __global__ void __launch_bounds__(kPullThreads)
   }
   degsum = warp_sum(degsum);
   if (lane == 0 && cnt) atomicAdd(packed, (static_cast<unsigned long long>(cnt) << kPackShift) | degsum);
+}
+
+template <class G, class Op, bool kEarly>
+__global__ void __launch_bounds__(kPullThreads)
+    pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
+           unsigned long long* packed) {
+  pull_words<G, Op, kEarly>(g, fb, op, nb, nwords, packed);
 }
 
 }  // namespace gbg
