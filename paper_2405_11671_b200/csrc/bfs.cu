@@ -134,7 +134,7 @@ __device__ void coop_bitmap_to_list(cooperative_groups::grid_group& grid, G g, c
 }
 
 template <class G>
-__global__ void __launch_bounds__(kPushThreads) bfs_coop_k(G g, CoopState s) {
+__global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   __shared__ uint32_t s_idx[kPushTile];
   __shared__ uint64_t s_red[33];
