@@ -93,7 +93,6 @@ struct CoopState {
   uint64_t* blocksum;          // [gridDim] conversion scan scratch
   uint64_t* result;            // [0] levels, [1] reached
   uint64_t nw;
-  const uint32_t* fnbr;        // first neighbour per vertex (read-only)
   double threshold;            // (1/20) * m, evaluated on the host like traversal.cpp:105-106
   uint32_t src;
 };
@@ -181,7 +180,7 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     BfsOp op{s.visited, s.depth, level};
     unsigned long long* acc = s.packed + level % 3;
     if (dense) {
-      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc, s.fnbr);
+      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc);
       has_list = false;
     } else {
       if (!has_list) {
@@ -273,7 +272,7 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
       cur.has_bm = true;
     }
     GBG_LAUNCH(g, (pull_k<G, Op, kEarly>), pull_grid(g, tb.nw), kPullThreads, 0, view, cur.bm, op, out.bm, tb.nw,
-               tb.packed, first_neighbors(g, view));
+               tb.packed);
     out.has_bm = true;
   } else {
     ensure_list(g, view, tb, cur);
@@ -321,7 +320,6 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.nw = tb.nw;
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
   s.src = src;
-  s.fnbr = first_neighbors(g, view);
   void* args[] = {&view, &s};
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));

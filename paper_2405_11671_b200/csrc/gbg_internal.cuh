@@ -178,7 +178,6 @@ struct gbg_graph {
   uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
   bool voff_valid = false;
   gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
-  uint32_t* fnbr = nullptr;     // cached first neighbour per vertex (BFS pull), 0xffffffff if none
 
   gbg::Workspace ws;
   // pinned host staging for small device->host scalars

@@ -481,8 +481,6 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
 void gbg_graph::invalidate_derived() {
   delete pr;
   pr = nullptr;
-  gbg::dfree(fnbr);
-  fnbr = nullptr;
   voff_valid = false;
 }
 

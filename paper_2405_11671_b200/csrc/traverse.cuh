@@ -202,12 +202,9 @@ constexpr uint32_t kPullSerial = 8;  // neighbours a lane scans before the warp 
 // at the first hit in list order when early exit applies.
 __device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
 
-// `fnbr` (optional, read-only): each vertex's first neighbour, so the most
-// frequent exit — a hit on the first (lowest-id, usually hub) neighbour —
-// costs a coalesced 4-byte read instead of a random 32-byte sector.
 template <class G, class Op, bool kEarly>
 __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
-                                           unsigned long long* packed, const uint32_t* fnbr) {
+                                           unsigned long long* packed) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -223,7 +220,7 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
       g.seg(v, b, d);
       const uint32_t lim = d < kPullSerial ? d : kPullSerial;
       for (uint32_t j = 0; j < lim; ++j) {
-        const uint32_t u = (j == 0 && fnbr) ? __ldg(fnbr + v) : g.at(b + j);
+        const uint32_t u = g.at(b + j);
         if (frontier_bit(fb, u) && op.update(u, v)) {
           found = true;
           if (kEarly) break;
@@ -274,30 +271,8 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
 template <class G, class Op, bool kEarly>
 __global__ void __launch_bounds__(kPullThreads)
     pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
-           unsigned long long* packed, const uint32_t* __restrict__ fnbr) {
-  pull_words<G, Op, kEarly>(g, fb, op, nb, nwords, packed, fnbr);
-}
-
-template <class G>
-__global__ void first_neighbor_k(G g, uint32_t* out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.n; v += stride) {
-    uint64_t b;
-    uint32_t d;
-    g.seg(static_cast<uint32_t>(v), b, d);
-    out[v] = d ? g.at(b) : 0xffffffffu;
-  }
-}
-
-// the cached first-neighbour array of a handle (built on first use,
-// dropped by updates with the other derived structures)
-template <class G>
-const uint32_t* first_neighbors(gbg_graph* g, G view) {
-  if (!g->fnbr) {
-    g->fnbr = dalloc<uint32_t>(g->n + 1);
-    GBG_LAUNCH(g, first_neighbor_k<G>, grid_for(g->n, 256), 256, 0, view, g->fnbr);
-  }
-  return g->fnbr;
+           unsigned long long* packed) {
+  pull_words<G, Op, kEarly>(g, fb, op, nb, nwords, packed);
 }
 
 }  // namespace gbg
