@@ -33,5 +33,17 @@ __device__ __forceinline__ double ld_keep_f64(const double* a, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
   return v;
 }
+// hot gathers: keep in L1 as well; cold gathers: do not allocate in L1 (so
+// they cannot evict the hot lines)
+__device__ __forceinline__ double ld_hot_f64(const double* a, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_cold_f64(const double* a, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
 
 }  // namespace gbg

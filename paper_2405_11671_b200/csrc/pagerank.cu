@@ -42,6 +42,9 @@ namespace gbg {
 
 constexpr int kPrThreads = 256;
 constexpr uint32_t kChunk = 4096;  // edges per heavy-row chunk (16 per thread)
+// Gathers of the kL1Hot highest-degree vertices (128 KiB of contribs, ~28%
+// of all gathers at scale 24) may stay in L1; the rest bypass it.
+constexpr uint32_t kL1Hot = 16384;
 // Degree classes over the degree-descending rows: class c gives each row
 // T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
 // at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
@@ -275,7 +278,8 @@ __device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint64
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const uint64_t k = t + static_cast<uint64_t>(j) * T;
-    const double x = k < d ? ld_keep_f64(a.x_old + ids[j], pl) : 0.0;
+    double x = 0.0;
+    if (k < d) x = ids[j] < kL1Hot ? ld_hot_f64(a.x_old + ids[j], pl) : ld_cold_f64(a.x_old + ids[j], pl);
     acc += fmax(x, 0.0);
   }
   return acc;
