@@ -1,0 +1,128 @@
+"""GPU edge cases the reference tests or its contract imply: empty and
+singleton graphs, very deep BFS (more levels than the stats window), hub
+rows far above every load-balancing threshold, disconnected pieces, and
+degenerate update batches.  Everything is compared with the C oracle."""
+import numpy as np
+import pytest
+
+from tests.helpers import csr, undirected
+
+pytestmark = pytest.mark.gpu
+TINY = np.finfo(np.float64).tiny
+
+
+def rel_l1(a, b):
+    return float(np.abs(a - b).sum() / max(np.abs(b).sum(), 1e-300))
+
+
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
+def test_empty_and_singleton_graphs(gbg, kind):
+    mk = gbg.CsrGraph.build if kind == "csr" else gbg.BlockedGraph.build
+    g0 = mk(0, [])
+    assert g0.num_vertices() == 0 and g0.num_edges() == 0
+    assert gbg.pagerank(g0).size == 0 and gbg.cc(g0).size == 0
+    with pytest.raises(IndexError):
+        gbg.bfs(g0, 0)
+    g1 = mk(1, [])
+    assert gbg.bfs(g1, 0).depth.tolist() == [0]
+    assert gbg.cc(g1).tolist() == [0]
+    assert np.allclose(gbg.pagerank(g1, 0.85, 20, TINY), [1.0])
+    assert gbg.triangle_count(g1) == 0
+
+
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
+def test_deep_path_bfs(gbg, orc, kind):
+    """A 3000-vertex path: 2999 levels, far beyond GBG_MAX_LEVELS."""
+    n = 3000
+    nn, pairs = undirected(n, [(i, i + 1) for i in range(n - 1)], orc)
+    off, nbr = csr(nn, pairs)
+    g = gbg.CsrGraph.build(nn, pairs) if kind == "csr" else gbg.BlockedGraph.build(nn, pairs)
+    for src in (0, 1234, n - 1):
+        r = gbg.bfs(g, src)
+        want, modes, sizes = orc.bfs(nn, off, nbr, src)
+        assert np.array_equal(r.depth, want)
+        assert r.reached == n
+        k = min(len(modes), 64)
+        assert r.modes[:k] == modes[:k] and r.frontier_sizes[:k] == sizes[:k]
+    assert gbg.cc(g).tolist() == [0] * n
+    assert rel_l1(gbg.pagerank(g, 0.85, 20, TINY), orc.pagerank(nn, off, nbr, 0.85, 20, TINY)) <= 1e-9
+
+
+def test_huge_star_and_disconnected_pieces(gbg, orc):
+    """One hub of 200k leaves (far above every split threshold) plus a
+    triangle and isolated vertices."""
+    leaves = 200_000
+    edges = [(0, v) for v in range(1, leaves + 1)] + [(leaves + 1, leaves + 2), (leaves + 2, leaves + 3),
+                                                        (leaves + 1, leaves + 3)]
+    n = leaves + 10
+    nn, pairs = undirected(n, edges, orc)
+    off, nbr = csr(nn, pairs)
+    g = gbg.CsrGraph.build(nn, pairs)
+    for src in (0, 5, leaves + 2, leaves + 7):
+        assert np.array_equal(gbg.bfs(g, src).depth, orc.bfs(nn, off, nbr, src)[0])
+    assert np.array_equal(gbg.cc(g), orc.cc(nn, off, nbr))
+    assert gbg.triangle_count(g) == 1
+    assert rel_l1(gbg.pagerank(g, 0.85, 20, TINY), orc.pagerank(nn, off, nbr, 0.85, 20, TINY)) <= 1e-9
+    # early convergence: the tolerance break (algorithms.cpp:552)
+    for tol in (1e-3, 1e-6):
+        assert rel_l1(gbg.pagerank(g, 0.85, 100, tol), orc.pagerank(nn, off, nbr, 0.85, 100, tol)) <= 1e-9
+
+
+def test_complete_graph(gbg, orc):
+    k = 300
+    nn, pairs = undirected(k, [(i, j) for i in range(k) for j in range(i + 1, k)], orc)
+    g = gbg.CsrGraph.build(nn, pairs)
+    d = gbg.bfs(g, 7).depth
+    assert d[7] == 0 and set(d.tolist()) == {0, 1}
+    assert np.allclose(gbg.pagerank(g, 0.85, 20, TINY), 1.0 / k, rtol=1e-12, atol=0)
+    assert gbg.triangle_count(g) == k * (k - 1) * (k - 2) // 6
+
+
+def test_degenerate_batches(gbg, orc):
+    edges = [(i, (i * 7 + 3) % 64) for i in range(64)]
+    n, pairs = undirected(64, edges, orc)
+    g = gbg.BlockedGraph.build(n, pairs)
+    off, nbr = csr(n, pairs)
+
+    def expect(batch, insert):
+        nonlocal off, nbr
+        k, off, nbr = orc.set_apply(n, off, nbr, orc.prepare_global(batch), insert)
+        return k
+
+    assert g.insert_batch(np.zeros((0, 2), np.uint32)) == 0
+    assert g.insert_batch([[5, 5], [9, 9]]) == 0  # only self-loops (batch.cpp:36)
+    assert g.insert_batch(pairs) == 0              # all present
+    b = [[1, 2], [1, 2], [1, 2]]                  # duplicates of one arc
+    assert g.delete_batch(b) == expect(b, False)
+    dup = np.array([[10, 20]] * 1000 + [[20, 10]] * 1000, np.uint32)
+    ins = g.insert_batch(dup)
+    assert ins == expect(dup, True) and g.num_edges() == int(off[n])
+    assert g.delete_batch(dup) == expect(dup, False) == ins
+    with pytest.raises(IndexError):
+        g.insert_batch([[0, 64]])
+    assert g.num_edges() == int(off[n])
+    # delete everything, then insert everything back
+    off, nbr = g.to_csr()
+    allp = np.stack([np.repeat(np.arange(n, dtype=np.uint32), np.diff(off.astype(np.int64))), nbr], axis=1)
+    assert g.delete_batch(allp) == allp.shape[0] and g.num_edges() == 0
+    assert g.insert_batch(allp) == allp.shape[0]
+    o2, n2 = g.to_csr()
+    assert np.array_equal(o2, off) and np.array_equal(n2, nbr)
+
+
+def test_pool_growth_and_relayout(gbg, orc):
+    """Insert far more arcs than the initial pool holds (forces grown lists
+    and a relayout into a larger pool), then delete them again."""
+    n = 5000
+    g = gbg.BlockedGraph.build(n, [])
+    rng = np.random.default_rng(3)
+    off, nbr = csr(n, np.zeros((0, 2), np.uint32))
+    for step in range(6):
+        raw = rng.integers(0, n, size=(200_000, 2)).astype(np.uint32)
+        raw[: 50_000, 0] = step  # a few fast-growing hubs
+        want, off, nbr = orc.set_apply(n, off, nbr, orc.prepare_global(raw), True)
+        assert g.insert_batch(raw) == want
+    go, gn = g.to_csr()
+    assert np.array_equal(go, off) and np.array_equal(gn, nbr)
+    assert np.array_equal(gbg.bfs(g, 0).depth, orc.bfs(n, off, nbr, 0)[0])
+    assert g.memory_bytes() > 0
