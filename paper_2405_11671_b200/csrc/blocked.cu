@@ -337,7 +337,9 @@ __global__ void refresh_caps_k(uint64_t n, const uint32_t* deg, uint32_t* cap) {
 
 // prepare(GlobalSort) on the device; returns the unique, self-loop-free
 // keys (sorted) and their count.
-uint64_t prepare_device(gbg_graph* g, const uint32_t* pairs, uint64_t count, BatchKeys bk, uint64_t** ukeys_out) {
+// *free_out receives the other key buffer (free scratch afterwards).
+uint64_t prepare_device(gbg_graph* g, const uint32_t* pairs, uint64_t count, BatchKeys bk, uint64_t** ukeys_out,
+                        uint64_t** free_out) {
   uint64_t* keys = g->ws.get<uint64_t>("upd.keys", count);
   uint64_t* sorted = g->ws.get<uint64_t>("upd.sorted", count);
   int* bad = g->ws.get<int>("upd.bad", 1);
@@ -346,8 +348,10 @@ uint64_t prepare_device(gbg_graph* g, const uint32_t* pairs, uint64_t count, Bat
   int hb = 0;
   read_scalars(g, bad, sizeof(hb), &hb);
   if (hb) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
-  const uint64_t U = sort_unique_keys(g, keys, sorted, count, bk, keys, "upd");
-  *ukeys_out = keys;
+  uint64_t U = 0;
+  uint64_t* uk = sort_unique_keys(g, keys, sorted, count, bk, &U, "upd");
+  *ukeys_out = uk;
+  *free_out = uk == keys ? sorted : keys;
   return U;
 }
 
@@ -359,10 +363,10 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   if (count > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "batch too large (max 2^32-1 arcs)");
   const BatchKeys bk{key_bits(g->n)};
   uint64_t* ukeys = nullptr;
-  const uint32_t U = static_cast<uint32_t>(prepare_device(g, pairs_dev, count, bk, &ukeys));
+  uint64_t* akeys = nullptr;  // the free key buffer receives the applied arcs
+  const uint32_t U = static_cast<uint32_t>(prepare_device(g, pairs_dev, count, bk, &ukeys, &akeys));
   if (U == 0) return 0;
   uint32_t* cnt = g->ws.get<uint32_t>("upd.cnt", 4);
-  uint64_t* akeys = g->ws.get<uint64_t>("upd.sorted", count);  // sorted buffer is free now
   uint32_t* flag = g->ws.get<uint32_t>("upd.flag", U);
   uint32_t* lb = g->ws.get<uint32_t>("upd.lb", U);
   uint32_t* alb = g->ws.get<uint32_t>("upd.alb", U);

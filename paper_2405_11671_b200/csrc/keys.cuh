@@ -7,9 +7,7 @@
 // (types.hpp:21-25), so sorting keys == std::sort on Edges.
 #pragma once
 
-#include <cub/device/device_radix_sort.cuh>
-
-#include "scan.cuh"
+#include "radix.cuh"
 
 namespace gbg {
 
@@ -52,22 +50,18 @@ struct UniqueOut {
   }
 };
 
-// LSD radix sort of `count` keys over 2L bits (CUB onesweep), then unique.
-// keys_in is clobbered; returns the unique count, result in *out.
-inline uint64_t sort_unique_keys(gbg_graph* g, uint64_t* keys_in, uint64_t* scratch, uint64_t count, BatchKeys bk,
-                                 uint64_t* out, const char* tag) {
-  size_t temp = 0;
-  GBG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, keys_in, scratch, count, 0, 2 * bk.L, g->stream));
-  void* tmp = g->ws.get(std::string(tag) + ".cubtmp", temp);
-  GBG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, temp, keys_in, scratch, count, 0, 2 * bk.L, g->stream));
-  g->launches += static_cast<uint64_t>((2 * bk.L + 7) / 8) + 1;
+// Stable LSD radix sort of `count` keys over 2L bits (radix.cuh), then
+// unique.  a and b are both clobbered; returns the buffer (a or b) that
+// holds the *U_out unique keys — the other one is free scratch afterwards.
+inline uint64_t* sort_unique_keys(gbg_graph* g, uint64_t* a, uint64_t* b, uint64_t count, BatchKeys bk,
+                                  uint64_t* U_out, const char* tag) {
+  uint64_t* sorted = radix_sort_u64(g, a, b, count, 2 * bk.L, tag);
+  uint64_t* other = sorted == a ? b : a;
   uint64_t* cnt = g->ws.get<uint64_t>(std::string(tag) + ".ucnt", 1);
-  device_scan<uint64_t>(g, UniqueIn{scratch, bk}, UniqueOut{scratch, bk, out}, count, cnt,
+  device_scan<uint64_t>(g, UniqueIn{sorted, bk}, UniqueOut{sorted, bk, other}, count, cnt,
                         (std::string(tag) + ".uniq").c_str());
-  uint64_t U = 0;
-  read_scalars(g, cnt, sizeof(U), &U);
-  g->ws.release(std::string(tag) + ".cubtmp");
-  return U;
+  read_scalars(g, cnt, sizeof(*U_out), U_out);
+  return other;
 }
 
 }  // namespace gbg

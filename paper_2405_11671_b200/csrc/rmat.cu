@@ -130,12 +130,13 @@ gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, d
       uint64_t* scratch = dalloc<uint64_t>(count);
       try {
         if (arcs) GBG_LAUNCH(g.get(), rmat_keys_k, grid_for(arcs, 256, g->sm_count * 16), 256, 0, p, arcs, bk, keys);
-        m = arcs ? sort_unique_keys(g.get(), keys, scratch, count, bk, keys, "rmat") : 0;
+        uint64_t* uniq = keys;
+        if (arcs) uniq = sort_unique_keys(g.get(), keys, scratch, count, bk, &m, "rmat");
         g->m = m;
         g->off = dalloc<uint64_t>(n + 1);
         g->nbr = dalloc<uint32_t>(m);
-        uint32_t* src = reinterpret_cast<uint32_t*>(scratch);  // scratch is free after unique
-        if (m) GBG_LAUNCH(g.get(), split_keys_k, grid_for(m, 256, g->sm_count * 16), 256, 0, keys, m, bk, src, g->nbr);
+        uint32_t* src = reinterpret_cast<uint32_t*>(uniq == keys ? scratch : keys);  // the free buffer
+        if (m) GBG_LAUNCH(g.get(), split_keys_k, grid_for(m, 256, g->sm_count * 16), 256, 0, uniq, m, bk, src, g->nbr);
         build_csr_offsets_from_sorted_src(g.get(), src, m, g->off);
         GBG_CUDA(cudaStreamSynchronize(g->stream));
       } catch (...) {
