@@ -25,6 +25,7 @@ constexpr int kSortRounds = 16;
 constexpr uint32_t kSortTile = kSortThreads * kSortRounds;  // 4096 keys
 constexpr int kRadixBits = 8;
 constexpr uint32_t kRadix = 1u << kRadixBits;
+static_assert(kSortThreads == static_cast<int>(kRadix), "one thread per digit in the tile scan");
 
 static __global__ void __launch_bounds__(kSortThreads) radix_hist_k(const uint64_t* __restrict__ keys, uint64_t n, int shift,
                                                              uint32_t ntiles, uint32_t* __restrict__ counts) {
@@ -44,76 +45,67 @@ static __global__ void __launch_bounds__(kSortThreads) radix_hist_k(const uint64
 static __global__ void __launch_bounds__(kSortThreads) radix_scatter_k(const uint64_t* __restrict__ in,
                                                                 uint64_t* __restrict__ out, uint64_t n, int shift,
                                                                 uint32_t ntiles, const uint32_t* __restrict__ offs) {
+  constexpr int kWarps = kSortThreads / 32;
+  constexpr uint32_t kSub = kSortTile / kWarps;  // 512 consecutive keys per warp
   __shared__ uint64_t s_keys[kSortTile];
-  __shared__ uint32_t s_base[kRadix];       // global slot of this tile's first key of each digit
-  __shared__ uint32_t s_start[kRadix];      // first slot of each digit inside the digit-sorted tile
-  __shared__ uint32_t s_run[kRadix];        // keys of each digit ranked so far (earlier rounds)
-  __shared__ uint32_t s_wcnt[kSortThreads / 32][kRadix];
+  __shared__ uint32_t s_base[kRadix];    // global slot of this tile's first key of each digit
+  __shared__ uint32_t s_start[kRadix];   // first slot of each digit inside the digit-sorted tile
+  __shared__ uint32_t s_cnt[kWarps][kRadix];  // per-warp digit counts, then per-warp running slots
+  __shared__ uint32_t s_red[33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kSortTile;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kSortTile + static_cast<uint64_t>(warp) * kSub;
+  const uint32_t lt = (1u << lane) - 1;
 
-  // tile histogram -> exclusive start of each digit inside the tile
-  for (uint32_t d = threadIdx.x; d < kRadix; d += kSortThreads) {
-    s_run[d] = 0;
-    s_base[d] = offs[d * ntiles + blockIdx.x];
-  }
-  __syncthreads();
+  for (uint32_t x = lane; x < kRadix; x += 32) s_cnt[warp][x] = 0;
+  for (uint32_t d = threadIdx.x; d < kRadix; d += kSortThreads) s_base[d] = offs[d * ntiles + blockIdx.x];
+  __syncwarp();
+  // 1. each warp: its keys (coalesced, kept in registers) and digit counts
   uint64_t k[kSortRounds];
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
-    const uint64_t i = base + r * kSortThreads + threadIdx.x;
-    k[r] = i < n ? in[i] : ~0ull;
-    if (i < n) atomicAdd(&s_run[(k[r] >> shift) & (kRadix - 1)], 1u);
+    const uint64_t i = base + r * 32 + lane;
+    const bool valid = i < n;
+    k[r] = valid ? in[i] : ~0ull;
+    const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
+    __syncwarp();
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    // exclusive scan of the 256 tile counts by one warp (8 per lane)
-    uint32_t c[kRadix / 32], sum = 0;
+  // 2. digit totals -> tile start of each digit; per-warp start inside it
+  {
+    const uint32_t d = threadIdx.x;  // kSortThreads == kRadix
+    uint32_t tot = 0;
 #pragma unroll
-    for (int j = 0; j < static_cast<int>(kRadix / 32); ++j) {
-      c[j] = s_run[lane * (kRadix / 32) + j];
-      sum += c[j];
-    }
-    uint32_t inc = warp_inclusive_scan(sum), pre = inc - sum;
+    for (int w = 0; w < kWarps; ++w) tot += s_cnt[w][d];
+    uint32_t all;
+    const uint32_t start = block_exclusive_scan(tot, s_red, all);
+    s_start[d] = start;
+    uint32_t run = start;
 #pragma unroll
-    for (int j = 0; j < static_cast<int>(kRadix / 32); ++j) {
-      s_start[lane * (kRadix / 32) + j] = pre;
-      pre += c[j];
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_cnt[w][d];
+      s_cnt[w][d] = run;
+      run += c;
     }
   }
   __syncthreads();
-  for (uint32_t d = threadIdx.x; d < kRadix; d += kSortThreads) s_run[d] = 0;
-
-  // stable ranks, round by round (tile order = round-major, thread-minor)
-  const uint32_t lt = (1u << lane) - 1;
+  // 3. each warp ranks its keys in order (stable) into the staged tile
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
-    const uint64_t i = base + r * kSortThreads + threadIdx.x;
-    const bool valid = i < n;
+    const bool valid = base + r * 32 + lane < n;
     const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
-    for (uint32_t x = lane; x < kRadix; x += 32) s_wcnt[warp][x] = 0;
-    __syncwarp();
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t rank_w = __popc(peers & lt);
-    if (valid && rank_w == 0) s_wcnt[warp][d] = __popc(peers);
-    __syncthreads();
-    if (valid) {
-      uint32_t pre = 0;
-      for (int w = 0; w < warp; ++w) pre += s_wcnt[w][d];
-      s_keys[s_start[d] + s_run[d] + pre + rank_w] = k[r];
-    }
-    __syncthreads();
-    for (uint32_t x = threadIdx.x; x < kRadix; x += kSortThreads) {
-      uint32_t t = 0;
-#pragma unroll
-      for (int w = 0; w < kSortThreads / 32; ++w) t += s_wcnt[w][x];
-      s_run[x] += t;
-    }
-    __syncthreads();
+    if (valid) s_keys[s_cnt[warp][d] + __popc(peers & lt)] = k[r];
+    __syncwarp();
+    if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
+    __syncwarp();
   }
-  // coalesced write-out: slot j of the digit-sorted tile goes to
+  __syncthreads();
+  // 4. coalesced write-out: slot j of the digit-sorted tile goes to
   // s_base[digit] + (j - s_start[digit])
-  const uint32_t len = static_cast<uint32_t>(n - base < kSortTile ? n - base : kSortTile);
+  const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSortTile;
+  const uint32_t len = static_cast<uint32_t>(n - tile0 < kSortTile ? n - tile0 : kSortTile);
   for (uint32_t j = threadIdx.x; j < len; j += kSortThreads) {
     const uint64_t key = s_keys[j];
     const uint32_t d = static_cast<uint32_t>((key >> shift) & (kRadix - 1));
