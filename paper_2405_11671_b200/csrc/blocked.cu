@@ -349,7 +349,9 @@ uint64_t prepare_device(gbg_graph* g, const uint32_t* pairs, uint64_t count, Bat
   read_scalars(g, bad, sizeof(hb), &hb);
   if (hb) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
   uint64_t U = 0;
+  PhaseTrace tr(g->stream, "prepare");
   uint64_t* uk = sort_unique_keys(g, keys, sorted, count, bk, &U, "upd");
+  tr.mark("sort+unique");
   *ukeys_out = uk;
   *free_out = uk == keys ? sorted : keys;
   return U;
@@ -362,9 +364,11 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   if (count == 0) return 0;
   if (count > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "batch too large (max 2^32-1 arcs)");
   const BatchKeys bk{key_bits(g->n)};
+  PhaseTrace tr(g->stream, insert ? "insert_batch" : "delete_batch");
   uint64_t* ukeys = nullptr;
   uint64_t* akeys = nullptr;  // the free key buffer receives the applied arcs
   const uint32_t U = static_cast<uint32_t>(prepare_device(g, pairs_dev, count, bk, &ukeys, &akeys));
+  tr.mark("prepare");
   if (U == 0) return 0;
   uint32_t* cnt = g->ws.get<uint32_t>("upd.cnt", 4);
   uint32_t* flag = g->ws.get<uint32_t>("upd.flag", U);
@@ -382,6 +386,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint32_t ng = 0;
   read_scalars(g, cnt + 2, sizeof(ng), &ng);
   GBG_CUDA(cudaMemcpyAsync(gstart + ng, &A, sizeof(A), cudaMemcpyHostToDevice, g->stream));  // gstart[ng] = A
+  tr.mark("presence+groups");
   uint32_t* gcnt = g->ws.get<uint32_t>("upd.gcnt", ng);
   uint32_t* gnewdeg = g->ws.get<uint32_t>("upd.gnewdeg", ng);
   uint32_t* gnewcap = g->ws.get<uint32_t>("upd.gnewcap", ng);
@@ -410,7 +415,9 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint64_t otot = 0;
   read_scalars(g, oscan + ng, sizeof(otot), &otot);
   uint32_t* staged = g->ws.get<uint32_t>("upd.staged", otot);
+  tr.mark("plan");
   expand(g, oscan, ng, otot, StageOp{gsrc, g->bstart, g->pool, staged});
+  tr.mark("stage");
   // destinations
   uint64_t* newstart = g->ws.get<uint64_t>("upd.newstart", g->n);
   GBG_LAUNCH(g, plan_dest_k, grid_for(ng, 256), 256, 0, ng, gsrc, gascan, galloc, g->pool_top, g->bstart, newstart);
@@ -418,6 +425,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   if (insert) expand(g, gstart, ng, A, MergeNewOp{gsrc, akeys, alb, bk, newstart, g->pool});
   GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,
              g->bcap);
+  tr.mark("merge");
   uint64_t need = 0;
   read_scalars(g, gascan + ng, sizeof(need), &need);
   g->pool_top += need;

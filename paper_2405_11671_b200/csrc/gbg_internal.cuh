@@ -6,10 +6,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/gbg_c.h"
 
@@ -221,6 +225,43 @@ void with_view(gbg_graph* g, F&& f) {
 // Ensure the blocked container's virtual offsets (scan of degrees) are
 // current; returns a pointer usable as CSR-like offsets for scheduling.
 const uint64_t* virtual_offsets(gbg_graph* g);
+
+// Optional phase timing (environment GBG_TRACE=1): CUDA events on the
+// handle's stream at named points, device-time deltas printed to stderr
+// when the tracer goes out of scope.
+struct PhaseTrace {
+  cudaStream_t stream;
+  const char* what;
+  bool on;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  PhaseTrace(cudaStream_t s, const char* w) : stream(s), what(w), on(enabled()) { mark("start"); }
+  static bool enabled() {
+    static const bool e = [] {
+      const char* v = std::getenv("GBG_TRACE");
+      return v && v[0] == '1';
+    }();
+    return e;
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    marks.emplace_back(name, e);
+  }
+  ~PhaseTrace() {
+    if (!on || marks.empty()) return;
+    cudaEventSynchronize(marks.back().second);
+    std::fprintf(stderr, "[gbg trace] %s:", what);
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+      std::fprintf(stderr, " %s %.3f", marks[i].first, ms);
+    }
+    std::fprintf(stderr, " ms\n");
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+};
 
 }  // namespace gbg
 
