@@ -390,10 +390,11 @@ def main():
     nbr_p = torch.from_numpy(nbr.view(np.int32)).pin_memory()
     off_h = off_p.numpy().view(np.uint64)
     nbr_h = nbr_p.numpy().view(np.uint32)
+    ranks_h = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
 
     def e2e_step():
         h = gbg.CsrGraph.from_csr(off_h, nbr_h)
-        gbg.pagerank(h, 0.85, 20, TINY)
+        gbg.pagerank(h, 0.85, 20, TINY, out=ranks_h)
         del h
 
     e2e_step()

@@ -404,10 +404,14 @@ def bfs_device(g: _Graph, source: int, depth_ptr: int) -> dict:
     return _stats(st)
 
 
-def pagerank(g: _Graph, damping: float = 0.85, max_iters: int = 20, tolerance: float = 1e-4):
+def pagerank(g: _Graph, damping: float = 0.85, max_iters: int = 20, tolerance: float = 1e-4, out=None):
     """gb::pagerank (algorithms.cpp:508-555), fp64.  AlgoParams defaults
-    (algorithms.hpp:16-18)."""
-    out = np.empty(g.num_vertices(), dtype=np.float64)
+    (algorithms.hpp:16-18).  `out`: optional host float64 array (pinned
+    memory makes the device->host copy run at link speed)."""
+    if out is None:
+        out = np.empty(g.num_vertices(), dtype=np.float64)
+    elif out.dtype != np.float64 or out.size != g.num_vertices() or not out.flags.c_contiguous:
+        raise InvalidArgument("out must be a contiguous float64 array of num_vertices() entries")
     it = C.c_uint64()
     _check(_L.gbg_pagerank(g.handle, damping, max_iters, tolerance, _p(out, _f64p), C.byref(it)))
     return out
