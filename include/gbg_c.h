@@ -174,6 +174,10 @@ gbg_status gbg_pagerank_prepare(gbg_graph* g, double* build_ms);
  * component. */
 gbg_status gbg_cc(gbg_graph* g, uint32_t* labels);
 gbg_status gbg_cc_device(gbg_graph* g, uint32_t* labels_dev);
+/* gb::bc (algorithms.cpp:60-103): single-source Brandes dependencies over
+ * the BFS levels; delta[n] fp64, 0 for unreached vertices. */
+gbg_status gbg_bc(gbg_graph* g, uint32_t source, double* delta);
+gbg_status gbg_bc_device(gbg_graph* g, uint32_t source, double* delta_dev);
 /* Triangle count (not in the reference): orient u->v iff
  * (deg u, u) < (deg v, v) (derive_filter, derive.hpp:48-61), count
  * |N+(u) ∩ N+(v)| over oriented arcs. */

@@ -265,6 +265,14 @@ class RefCsr:
         self.ref._check(self.ref.L.gbref_cc(self.h, ptr(out, _u32p)))
         return out
 
+    def bc(self, src):
+        """gb::bc (algorithms.cpp:60-103)."""
+        L = self.ref.L
+        L.gbref_bc.argtypes = [C.c_void_p, C.c_uint32, _f64p]
+        out = np.empty(self.n, dtype=np.float64)
+        self.ref._check(L.gbref_bc(self.h, src, ptr(out, _f64p)))
+        return out
+
     def edge_map(self, ids, cond_mask, mode, early_exit=True):
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
         cond = np.ascontiguousarray(cond_mask, dtype=np.uint8)
@@ -404,6 +412,16 @@ class Oracle:
         self.L.gbo_cc(n, ptr(np.ascontiguousarray(off, dtype=np.uint64), _u64p),
                       ptr(np.ascontiguousarray(nbr, dtype=np.uint32), _u32p), ptr(out, _u32p))
         return out
+
+    def bc(self, n, off, nbr, src):
+        L = self.L
+        L.gbo_bc.argtypes = [C.c_uint64, _u64p, _u32p, C.c_uint32, _f64p]
+        out = np.empty(max(n, 1), dtype=np.float64)
+        rc = L.gbo_bc(n, ptr(np.ascontiguousarray(off, dtype=np.uint64), _u64p),
+                      ptr(np.ascontiguousarray(nbr, dtype=np.uint32), _u32p), src, ptr(out, _f64p))
+        if rc:
+            raise IndexError("bc: source out of range")
+        return out[:n]
 
     def tc(self, n, off, nbr) -> int:
         return int(self.L.gbo_tc(n, ptr(np.ascontiguousarray(off, dtype=np.uint64), _u64p),

@@ -334,6 +334,46 @@ int gbo_pagerank(uint64_t n, const uint64_t* off, const uint32_t* nbr, double da
   return 0;
 }
 
+/* algorithms.cpp:60-103: single-source Brandes dependencies.  Path counts
+ * pulled level by level from the previous layer, dependencies pulled from
+ * the next layer in reverse level order, each sum in sorted-neighbour order.
+ * Unreached vertices get 0. */
+int gbo_bc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, double* delta) {
+  if (src >= n) return 1;
+  int32_t* dist = (int32_t*)malloc((n + 1) * sizeof(int32_t));
+  uint64_t levels = 0;
+  int32_t mode[1];
+  uint64_t size[1];
+  gbo_bfs(n, off, nbr, src, dist, mode, size, 0, &levels);
+  int32_t maxd = 0;
+  for (uint64_t v = 0; v < n; ++v)
+    if (dist[v] > maxd) maxd = dist[v];
+  double* sigma = (double*)calloc(n + 1, sizeof(double));
+  sigma[src] = 1.0;
+  for (int32_t d = 1; d <= maxd; ++d)
+    for (uint64_t v = 0; v < n; ++v) {
+      if (dist[v] != d) continue;
+      double t = 0.0;
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e)
+        if (dist[nbr[e]] == d - 1) t += sigma[nbr[e]];
+      sigma[v] = t;
+    }
+  for (uint64_t v = 0; v < n; ++v) delta[v] = 0.0;
+  for (int32_t d = maxd - 1; d >= 0; --d)
+    for (uint64_t v = 0; v < n; ++v) {
+      if (dist[v] != d) continue;
+      double t = 0.0;
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+        uint32_t w = nbr[e];
+        if (dist[w] == d + 1) t += (sigma[v] / sigma[w]) * (1.0 + delta[w]);
+      }
+      delta[v] = t;
+    }
+  free(dist);
+  free(sigma);
+  return 0;
+}
+
 /* algorithms.cpp:194-234 semantics: components labelled by their minimum
  * vertex id (union by smaller root, full compression at the end). */
 void gbo_cc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* lab) {

@@ -26,6 +26,7 @@ int gbo_bfs(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, 
 int gbo_pagerank(uint64_t n, const uint64_t* off, const uint32_t* nbr, double damping,
                  uint64_t iters, double tol, double* out);
 void gbo_cc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* labels);
+int gbo_bc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, double* delta);
 uint64_t gbo_tc(uint64_t n, const uint64_t* off, const uint32_t* nbr);
 
 void gbo_subset_to_dense(uint64_t n, const uint32_t* ids, uint64_t k, uint64_t* words);

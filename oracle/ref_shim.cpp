@@ -256,6 +256,15 @@ int gbref_pagerank(void* csr, double damping, uint64_t iters, double tol, double
   });
 }
 
+// gb::bc (algorithms.cpp:60-103): single-source Brandes dependencies
+int gbref_bc(void* csr, uint32_t src, double* out) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    std::vector<double> d = bc(view, src);
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+  });
+}
+
 int gbref_cc(void* csr, uint32_t* labels) {
   return guard([&] {
     GraphView view(*static_cast<CsrGraph*>(csr));

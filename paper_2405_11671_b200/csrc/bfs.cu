@@ -396,12 +396,113 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   }
 }
 
+// ---------------------------------------------------------------- betweenness
+// gb::bc (algorithms.cpp:60-103): BFS depths, vertices bucketed by depth,
+// then path counts pulled level by level from the previous layer and
+// dependencies pulled from the next layer in reverse level order.  One warp
+// per vertex of the level; each sum is a fixed shuffle tree.
+__global__ void level_count_k(const int32_t* depth, uint64_t n, uint32_t* cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+    if (depth[v] >= 0) atomicAdd(cnt + depth[v], 1u);
+}
+__global__ void level_scatter_k(const int32_t* depth, uint64_t n, uint32_t* cursor, uint32_t* list) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+    if (depth[v] >= 0) list[atomicAdd(cursor + depth[v], 1u)] = static_cast<uint32_t>(v);
+}
+
+template <class G, bool kSigma>
+__global__ void bc_level_k(G g, const uint32_t* list, uint32_t count, const int32_t* depth, int32_t d,
+                           double* sigma, double* delta) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = w0; i < count; i += nw) {
+    const uint32_t v = list[i];
+    uint64_t b;
+    uint32_t deg;
+    g.seg(v, b, deg);
+    double acc = 0.0;
+    const double sv = kSigma ? 0.0 : sigma[v];
+    for (uint32_t j = lane; j < deg; j += 32) {
+      const uint32_t u = g.at(b + j);
+      if (kSigma) {
+        if (depth[u] == d - 1) acc += sigma[u];
+      } else if (depth[u] == d + 1) {
+        acc += (sv / sigma[u]) * (1.0 + delta[u]);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) (kSigma ? sigma : delta)[v] = acc;
+  }
+}
+
+template <class G>
+void bc_run(gbg_graph* g, G view, uint32_t src, double* delta) {
+  const uint64_t n = g->n;
+  int32_t* depth = g->ws.get<int32_t>("bc.depth", n);
+  gbg_bfs_stats st;
+  bfs_run(g, view, src, depth, &st);
+  const uint64_t nlev = st.levels;  // depths 0 .. nlev-1
+  uint32_t* cnt = g->ws.get<uint32_t>("bc.cnt", nlev + 1);
+  uint32_t* list = g->ws.get<uint32_t>("bc.list", n);
+  double* sigma = g->ws.get<double>("bc.sigma", n);
+  GBG_CUDA(cudaMemsetAsync(cnt, 0, (nlev + 1) * sizeof(uint32_t), g->stream));
+  GBG_LAUNCH(g, level_count_k, grid_for(n, 256), 256, 0, depth, n, cnt);
+  std::vector<uint32_t> hc(nlev + 1), start(nlev + 1);
+  GBG_CUDA(cudaMemcpyAsync(hc.data(), cnt, (nlev + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+  GBG_CUDA(cudaStreamSynchronize(g->stream));
+  uint32_t run = 0;
+  for (uint64_t d = 0; d <= nlev; ++d) {
+    start[d] = run;
+    run += hc[d];
+  }
+  GBG_CUDA(cudaMemcpyAsync(cnt, start.data(), (nlev + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream));
+  GBG_LAUNCH(g, level_scatter_k, grid_for(n, 256), 256, 0, depth, n, cnt, list);
+  GBG_CUDA(cudaMemsetAsync(sigma, 0, n * sizeof(double), g->stream));
+  GBG_CUDA(cudaMemsetAsync(delta, 0, n * sizeof(double), g->stream));
+  const double one = 1.0;
+  GBG_CUDA(cudaMemcpyAsync(sigma + src, &one, sizeof(double), cudaMemcpyHostToDevice, g->stream));
+  auto grid = [&](uint32_t c) { return grid_for(static_cast<uint64_t>(c) * 32, 256, g->sm_count * 16); };
+  for (uint64_t d = 1; d < nlev; ++d)
+    if (hc[d])
+      GBG_LAUNCH(g, (bc_level_k<G, true>), grid(hc[d]), 256, 0, view, list + start[d], hc[d], depth,
+                 static_cast<int32_t>(d), sigma, delta);
+  for (uint64_t d = nlev; d-- > 0;)
+    if (hc[d] && d + 1 < nlev)
+      GBG_LAUNCH(g, (bc_level_k<G, false>), grid(hc[d]), 256, 0, view, list + start[d], hc[d], depth,
+                 static_cast<int32_t>(d), sigma, delta);
+}
+
 }  // namespace
 }  // namespace gbg
 
 using namespace gbg;
 
 extern "C" {
+
+gbg_status gbg_bc_device(gbg_graph* g, uint32_t source, double* delta_dev) {
+  return guard([&] {
+    GBG_HANDLE(g);
+    if (!delta_dev) fail(GBG_ERR_INVALID_ARGUMENT, "null output");
+    if (source >= g->n) fail(GBG_ERR_OUT_OF_RANGE, "bc: source out of range");  // algorithms.cpp:62
+    with_view(g, [&](auto view) { bc_run(g, view, source, delta_dev); });
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+gbg_status gbg_bc(gbg_graph* g, uint32_t source, double* delta) {
+  return guard([&] {
+    GBG_HANDLE(g);
+    if (!delta) fail(GBG_ERR_INVALID_ARGUMENT, "null output");
+    if (source >= g->n) fail(GBG_ERR_OUT_OF_RANGE, "bc: source out of range");
+    double* d = g->ws.get<double>("bc.delta", g->n);
+    with_view(g, [&](auto view) { bc_run(g, view, source, d); });
+    GBG_CUDA(cudaMemcpyAsync(delta, d, g->n * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
 
 gbg_status gbg_bfs_device(gbg_graph* g, uint32_t source, int32_t* depth_dev, gbg_bfs_stats* stats) {
   return guard([&] {

@@ -151,6 +151,8 @@ _SIGS = {
     "gbg_update_batch_device": [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _vp],
     "gbg_contains_device": [_vp, _vp, C.c_uint64, _vp],
     "gbg_pagerank_prepare": [_vp, _f64p],
+    "gbg_bc": [_vp, C.c_uint32, _f64p],
+    "gbg_bc_device": [_vp, C.c_uint32, _vp],
     "gbg_load_gbcsr1": [C.c_char_p, C.c_int, _gpp],
     "gbg_save_gbcsr1": [_vp, C.c_char_p],
 }
@@ -428,6 +430,17 @@ def pagerank_device(g: _Graph, out_ptr: int, damping=0.85, max_iters=20, toleran
     it = C.c_uint64()
     _check(_L.gbg_pagerank_device(g.handle, damping, max_iters, tolerance, out_ptr, C.byref(it)))
     return it.value
+
+
+def bc(g: _Graph, source: int) -> np.ndarray:
+    """gb::bc (algorithms.cpp:60-103): single-source Brandes dependencies."""
+    out = np.empty(g.num_vertices(), dtype=np.float64)
+    _check(_L.gbg_bc(g.handle, source, _p(out, _f64p)))
+    return out
+
+
+def bc_device(g: _Graph, source: int, out_ptr: int):
+    _check(_L.gbg_bc_device(g.handle, source, out_ptr))
 
 
 def cc(g: _Graph) -> np.ndarray:

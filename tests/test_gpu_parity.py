@@ -303,6 +303,28 @@ def test_cc_asymmetric_arcs(gbg, orc):
             assert np.array_equal(gbg.cc(g), orc.cc(n, off, nbr)), trial
 
 
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
+def test_bc_matches_oracle(gbg, ref, orc, kind):
+    """gb::bc; the reference's own differential check is |Δ| <= 1e-9 per
+    vertex (bench.cpp:234-241); large dependencies are compared relatively."""
+    mk = (lambda n, p: gbg.CsrGraph.build(n, p)) if kind == "csr" else (lambda n, p: gbg.BlockedGraph.build(n, p))
+    assert gbg.bc(mk(4, T4_PAIRS), 3).tolist() == [0.0, 0.0, 2.0, 3.0]
+    with pytest.raises(IndexError):
+        gbg.bc(mk(4, T4_PAIRS), 9)
+    for trial in range(12):
+        n, pairs = ref.er(150 + 50 * trial, 0.04, 300 + trial)
+        off, nbr = csr(n, pairs)
+        want = orc.bc(n, off, nbr, trial)
+        got = gbg.bc(mk(n, pairs), trial)
+        assert np.abs(got - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
+    for S in (12, 16):
+        n, pairs = ref.rmat(S, 16 << S, 1)
+        off, nbr = csr(n, pairs)
+        want = orc.bc(n, off, nbr, 0)
+        got = gbg.bc(mk(n, pairs), 0)
+        assert np.abs(got - want).max() <= 1e-9 * np.abs(want).max()
+
+
 def test_tc_known_answers(gbg, ref, orc):
     assert gbg.triangle_count(gbg.CsrGraph.build(4, T4_PAIRS)) == 1
     for k in (3, 5, 8, 12, 40):

@@ -222,6 +222,19 @@ def test_pagerank_matches_reference(ref, orc):
             assert np.abs(a - b).sum() <= 1e-12
 
 
+def test_bc_matches_reference(ref, orc):
+    # test_algorithms.cpp:57-66: from the pendant of T4
+    off, nbr = csr(4, T4_PAIRS)
+    assert orc.bc(4, off, nbr, 3).tolist() == ref.csr(4, off, nbr).bc(3).tolist() == [0.0, 0.0, 2.0, 3.0]
+    for trial in range(10):
+        n, pairs = ref.er(150, 0.04, 300 + trial)
+        off, nbr = csr(n, pairs)
+        assert np.array_equal(orc.bc(n, off, nbr, trial), ref.csr(n, off, nbr).bc(trial))
+    n, pairs = ref.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    assert np.array_equal(orc.bc(n, off, nbr, 0), ref.csr(n, off, nbr).bc(0))
+
+
 def test_tc_known_answers(orc):
     off, nbr = csr(4, T4_PAIRS)
     assert orc.tc(4, off, nbr) == 1
