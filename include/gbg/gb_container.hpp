@@ -222,6 +222,13 @@ inline std::vector<gb::VertexId> cc(const GpuGraph& g) {
   return l;
 }
 
+// gb::bc (algorithms.cpp:60-103)
+inline std::vector<double> bc(const GpuGraph& g, gb::VertexId source) {
+  std::vector<double> d(g.num_vertices());
+  check(gbg_bc(g.handle(), source, d.data()));
+  return d;
+}
+
 inline uint64_t triangle_count(const GpuGraph& g) {
   uint64_t t = 0;
   check(gbg_tc(g.handle(), &t));
@@ -236,6 +243,12 @@ inline const std::vector<gb::AlgorithmInfo>& gpu_algorithms() {
        [](const gb::GraphView& v, const gb::AlgoParams& p) {
          gb::CanonicalOutput out;
          out.ints = bfs_distances(device_of(v), p.source);
+         return out;
+       }},
+      {"bc",
+       [](const gb::GraphView& v, const gb::AlgoParams& p) {
+         gb::CanonicalOutput out;
+         out.reals = bc(device_of(v), p.source);
          return out;
        }},
       {"cc",
