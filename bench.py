@@ -209,6 +209,16 @@ def run_pagerank(torch, gbg, g, steps, warmup, iters=20):
     return t / steps, launches, out
 
 
+def host_time(fn, steps, warmup):
+    """Wall time of a synchronous host-API call (it ends with a stream sync)."""
+    for _ in range(warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = fn()
+    return (time.perf_counter() - t0) / steps, out
+
+
 def run_bfs(torch, gbg, g, src, steps, warmup):
     depth = torch.empty(g.num_vertices(), dtype=torch.int32, device="cuda")
     stats = {}
@@ -430,6 +440,14 @@ def main():
         tc_ = events_time(torch, g.stream(), lambda: gbg.cc_device(g, lab.data_ptr()), args.steps) / args.steps
         workloads[f"cc_s{S}"] = {"ms": tc_ * 1e3, "arcs_per_s": m / tc_,
                                  "components": int(np.unique(lab.cpu().numpy()).size)}
+        # §8(f) row 3 on the same graph, through the host API (result copied
+        # back to host memory inside the timed call)
+        for name, fn, summary in (("kcore", lambda: gbg.kcore(g), lambda o: {"max_core": int(o.max())}),
+                                  ("coloring", lambda: gbg.coloring(g), lambda o: {"colors": int(o.max()) + 1}),
+                                  ("mis", lambda: gbg.mis(g, 1), lambda o: {"size": int(o.sum())})):
+            t_alg, out = host_time(fn, max(1, min(args.steps, 3)), 1)
+            workloads[f"{name}_s{S}"] = {"ms": t_alg * 1e3, "arcs_per_s": m / t_alg, **summary(out)}
+            log(f"{name}_s{S}: {t_alg * 1e3:.1f} ms")
     del pr_out
     if rank == 0 and not args.no_secondary:
         # configs[1] exactly: PR s20; configs[3]: TC s20; configs[0]: BFS s16

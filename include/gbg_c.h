@@ -178,6 +178,18 @@ gbg_status gbg_cc_device(gbg_graph* g, uint32_t* labels_dev);
  * the BFS levels; delta[n] fp64, 0 for unreached vertices. */
 gbg_status gbg_bc(gbg_graph* g, uint32_t source, double* delta);
 gbg_status gbg_bc_device(gbg_graph* g, uint32_t source, double* delta_dev);
+/* gb::kcore (algorithms.cpp:330-374, buckets.cpp:7-59): coreness[n] under
+ * out-degree peeling (remaining degree of v drops when a peeled vertex has
+ * v as a neighbour).  Coreness is order-independent, so it is exact on any
+ * graph. */
+gbg_status gbg_kcore(gbg_graph* g, uint64_t* coreness);
+/* gb::coloring (algorithms.cpp:376-432): first-fit colours in
+ * largest-log-degree-first order, ties to the lower id.  Symmetric graphs
+ * only (GBG_ERR_INVALID_ARGUMENT otherwise). */
+gbg_status gbg_coloring(gbg_graph* g, uint32_t* colors);
+/* gb::mis (algorithms.cpp:434-504): in_set[n] 0/1, the lexicographically
+ * first MIS under (rng_u64(seed, 7, v), v).  Symmetric graphs only. */
+gbg_status gbg_mis(gbg_graph* g, uint64_t seed, uint8_t* in_set);
 /* Triangle count (not in the reference): orient u->v iff
  * (deg u, u) < (deg v, v) (derive_filter, derive.hpp:48-61), count
  * |N+(u) ∩ N+(v)| over oriented arcs. */

@@ -273,6 +273,30 @@ class RefCsr:
         self.ref._check(L.gbref_bc(self.h, src, ptr(out, _f64p)))
         return out
 
+    def kcore(self):
+        """gb::kcore (algorithms.cpp:330-374)."""
+        L = self.ref.L
+        L.gbref_kcore.argtypes = [C.c_void_p, _u64p]
+        out = np.empty(self.n, dtype=np.uint64)
+        self.ref._check(L.gbref_kcore(self.h, ptr(out, _u64p)))
+        return out
+
+    def coloring(self):
+        """gb::coloring (algorithms.cpp:376-432)."""
+        L = self.ref.L
+        L.gbref_coloring.argtypes = [C.c_void_p, _u32p]
+        out = np.empty(self.n, dtype=np.uint32)
+        self.ref._check(L.gbref_coloring(self.h, ptr(out, _u32p)))
+        return out
+
+    def mis(self, seed=1):
+        """gb::mis (algorithms.cpp:434-504)."""
+        L = self.ref.L
+        L.gbref_mis.argtypes = [C.c_void_p, C.c_uint64, _u8p]
+        out = np.empty(self.n, dtype=np.uint8)
+        self.ref._check(L.gbref_mis(self.h, seed, ptr(out, _u8p)))
+        return out
+
     def edge_map(self, ids, cond_mask, mode, early_exit=True):
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
         cond = np.ascontiguousarray(cond_mask, dtype=np.uint8)
@@ -333,6 +357,8 @@ class Oracle:
         L.gbo_hash_combine.argtypes = [C.c_uint64, C.c_uint64]
         L.gbo_rng_double.restype = C.c_double
         L.gbo_rng_double.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.gbo_rng_u64.restype = C.c_uint64
+        L.gbo_rng_u64.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
         L.gbo_update_batch.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                        C.c_uint64, _u32p]
         L.gbo_normalize.restype = C.c_uint64
@@ -421,6 +447,31 @@ class Oracle:
                       ptr(np.ascontiguousarray(nbr, dtype=np.uint32), _u32p), src, ptr(out, _f64p))
         if rc:
             raise IndexError("bc: source out of range")
+        return out[:n]
+
+    def rng_u64(self, seed, stream, counter) -> int:
+        return int(self.L.gbo_rng_u64(seed, stream, counter))
+
+    def _csr_args(self, off, nbr):
+        return (ptr(np.ascontiguousarray(off, dtype=np.uint64), _u64p),
+                ptr(np.ascontiguousarray(nbr, dtype=np.uint32), _u32p))
+
+    def kcore(self, n, off, nbr):
+        self.L.gbo_kcore.argtypes = [C.c_uint64, _u64p, _u32p, _u64p]
+        out = np.empty(max(n, 1), dtype=np.uint64)
+        self.L.gbo_kcore(n, *self._csr_args(off, nbr), ptr(out, _u64p))
+        return out[:n]
+
+    def coloring(self, n, off, nbr):
+        self.L.gbo_coloring.argtypes = [C.c_uint64, _u64p, _u32p, _u32p]
+        out = np.empty(max(n, 1), dtype=np.uint32)
+        self.L.gbo_coloring(n, *self._csr_args(off, nbr), ptr(out, _u32p))
+        return out[:n]
+
+    def mis(self, n, off, nbr, seed=1):
+        self.L.gbo_mis.argtypes = [C.c_uint64, _u64p, _u32p, C.c_uint64, _u8p]
+        out = np.empty(max(n, 1), dtype=np.uint8)
+        self.L.gbo_mis(n, *self._csr_args(off, nbr), seed, ptr(out, _u8p))
         return out[:n]
 
     def tc(self, n, off, nbr) -> int:

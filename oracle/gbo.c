@@ -20,10 +20,14 @@ uint64_t gbo_hash_combine(uint64_t a, uint64_t b) {
   return gbo_mix64(a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2)));
 }
 
-/* rng.hpp:22-29: top 53 bits of rng_u64 times 2^-53 */
+/* rng.hpp:22-24 */
+uint64_t gbo_rng_u64(uint64_t seed, uint64_t stream, uint64_t counter) {
+  return gbo_mix64(gbo_hash_combine(gbo_hash_combine(seed, stream), counter));
+}
+
+/* rng.hpp:27-29: top 53 bits of rng_u64 times 2^-53 */
 double gbo_rng_double(uint64_t seed, uint64_t stream, uint64_t counter) {
-  uint64_t r = gbo_mix64(gbo_hash_combine(gbo_hash_combine(seed, stream), counter));
-  return (double)(r >> 11) * 0x1.0p-53;
+  return (double)(gbo_rng_u64(seed, stream, counter) >> 11) * 0x1.0p-53;
 }
 
 /* batch.cpp:128-154: `size` recursive-quadrant draws, each emitted as (u,v)
@@ -464,4 +468,182 @@ uint64_t gbo_set_apply(uint64_t n, const uint64_t* off, const uint32_t* nbr, con
     off_out[v + 1] = w;
   }
   return applied;
+}
+
+/* algorithms.cpp:330-374 + buckets.cpp:7-59: peel the lowest bucket k;
+ * each peeled vertex decrements the remaining degree of the neighbours still
+ * in a bucket above k, which move to bucket max(k, remaining).  Restated as
+ * the serial bin-sort peel (vertices in nondecreasing remaining degree; a
+ * neighbour only drops while above the current level), which visits the
+ * same bucket sequence one vertex at a time. */
+void gbo_kcore(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t* core) {
+  if (!n) return;
+  uint64_t md = 0;
+  uint64_t* rem = (uint64_t*)malloc(n * sizeof(uint64_t));
+  for (uint64_t v = 0; v < n; ++v) {
+    rem[v] = off[v + 1] - off[v];
+    if (rem[v] > md) md = rem[v];
+  }
+  uint64_t* bin = (uint64_t*)calloc(md + 2, sizeof(uint64_t));
+  uint64_t* pos = (uint64_t*)malloc(n * sizeof(uint64_t));
+  uint32_t* vert = (uint32_t*)malloc(n * sizeof(uint32_t));
+  for (uint64_t v = 0; v < n; ++v) ++bin[rem[v]];
+  uint64_t start = 0;
+  for (uint64_t d = 0; d <= md; ++d) {
+    uint64_t c = bin[d];
+    bin[d] = start;
+    start += c;
+  }
+  for (uint64_t v = 0; v < n; ++v) {
+    pos[v] = bin[rem[v]]++;
+    vert[pos[v]] = (uint32_t)v;
+  }
+  for (uint64_t d = md; d > 0; --d) bin[d] = bin[d - 1];
+  bin[0] = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t v = vert[i];
+    core[v] = rem[v];
+    for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+      uint32_t u = nbr[e];
+      if (rem[u] > rem[v]) {
+        uint64_t du = rem[u], pu = pos[u], pw = bin[du];
+        uint32_t w = vert[pw];
+        if (u != w) {
+          pos[u] = pw;
+          vert[pw] = u;
+          pos[w] = pu;
+          vert[pu] = w;
+        }
+        ++bin[du];
+        --rem[u];
+      }
+    }
+  }
+  free(rem);
+  free(bin);
+  free(pos);
+  free(vert);
+}
+
+static unsigned gbo_bit_width(uint64_t x) {
+  unsigned b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+/* algorithms.cpp:376-432: waiting[v] = neighbours beating v (higher
+ * bit_width(degree), ties to the lower id); ready vertices take the smallest
+ * colour unused by the neighbours beating them, then release the others.
+ * Rounds run serially, in frontier order. */
+void gbo_coloring(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* colors) {
+  if (!n) return;
+  unsigned* llf = (unsigned*)malloc(n * sizeof(unsigned));
+  int64_t* waiting = (int64_t*)calloc(n, sizeof(int64_t));
+  uint32_t* cur = (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* nxt = (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint64_t md = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    uint64_t d = off[v + 1] - off[v];
+    llf[v] = gbo_bit_width(d);
+    if (d > md) md = d;
+    colors[v] = UINT32_MAX;
+  }
+#define GBO_BEATS(a, b) (llf[a] != llf[b] ? llf[a] > llf[b] : (a) < (b))
+  for (uint64_t v = 0; v < n; ++v)
+    for (uint64_t e = off[v]; e < off[v + 1]; ++e)
+      if (GBO_BEATS(nbr[e], (uint32_t)v)) ++waiting[v];
+  uint64_t nc = 0;
+  for (uint64_t v = 0; v < n; ++v)
+    if (waiting[v] == 0) cur[nc++] = (uint32_t)v;
+  unsigned char* used = (unsigned char*)malloc(md + 2);
+  while (nc) {
+    uint64_t nn = 0;
+    for (uint64_t i = 0; i < nc; ++i) {
+      uint32_t v = cur[i];
+      uint64_t d = off[v + 1] - off[v];
+      memset(used, 0, d + 1);
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+        uint32_t u = nbr[e];
+        if (GBO_BEATS(u, v) && colors[u] <= d) used[colors[u]] = 1;
+      }
+      uint32_t c = 0;
+      while (used[c]) ++c;
+      colors[v] = c;
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+        uint32_t u = nbr[e];
+        if (GBO_BEATS(u, v)) continue;
+        if (--waiting[u] == 0) nxt[nn++] = u;
+      }
+    }
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+    nc = nn;
+  }
+#undef GBO_BEATS
+  free(llf);
+  free(waiting);
+  free(cur);
+  free(nxt);
+  free(used);
+}
+
+/* algorithms.cpp:434-504: rank[v] = rng_u64(seed, 7, v), lower (rank, id)
+ * wins; joiners enter and knock their undecided neighbours out, then every
+ * vertex decided this round releases its undecided lower-priority
+ * neighbours; released vertices still undecided join next round. */
+void gbo_mis(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t seed, uint8_t* in_set) {
+  if (!n) return;
+  uint64_t* rank = (uint64_t*)malloc(n * sizeof(uint64_t));
+  int64_t* waiting = (int64_t*)calloc(n, sizeof(int64_t));
+  uint8_t* status = (uint8_t*)calloc(n, 1); /* 0 undecided, 1 in, 2 out */
+  uint32_t* join = (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* decided = (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* rel = (uint32_t*)malloc(n * sizeof(uint32_t));
+  for (uint64_t v = 0; v < n; ++v) rank[v] = gbo_rng_u64(seed, 7, v);
+#define GBO_BEATS(a, b) (rank[a] != rank[b] ? rank[a] < rank[b] : (a) < (b))
+  for (uint64_t v = 0; v < n; ++v)
+    for (uint64_t e = off[v]; e < off[v + 1]; ++e)
+      if (GBO_BEATS(nbr[e], (uint32_t)v)) ++waiting[v];
+  uint64_t nj = 0;
+  for (uint64_t v = 0; v < n; ++v)
+    if (waiting[v] == 0) join[nj++] = (uint32_t)v;
+  while (nj) {
+    uint64_t nd = 0;
+    for (uint64_t i = 0; i < nj; ++i) {
+      uint32_t v = join[i];
+      status[v] = 1;
+      decided[nd++] = v;
+    }
+    for (uint64_t i = 0; i < nj; ++i) {
+      uint32_t v = join[i];
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e)
+        if (status[nbr[e]] == 0) {
+          status[nbr[e]] = 2;
+          decided[nd++] = nbr[e];
+        }
+    }
+    uint64_t nr = 0;
+    for (uint64_t i = 0; i < nd; ++i) {
+      uint32_t v = decided[i];
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+        uint32_t u = nbr[e];
+        if (GBO_BEATS(v, u) && status[u] == 0 && --waiting[u] == 0) rel[nr++] = u;
+      }
+    }
+    nj = 0;
+    for (uint64_t i = 0; i < nr; ++i)
+      if (status[rel[i]] == 0) join[nj++] = rel[i];
+  }
+#undef GBO_BEATS
+  for (uint64_t v = 0; v < n; ++v) in_set[v] = status[v] == 1;
+  free(rank);
+  free(waiting);
+  free(status);
+  free(join);
+  free(decided);
+  free(rel);
 }

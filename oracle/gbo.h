@@ -11,6 +11,7 @@
 uint64_t gbo_mix64(uint64_t x);
 uint64_t gbo_hash_combine(uint64_t a, uint64_t b);
 double gbo_rng_double(uint64_t seed, uint64_t stream, uint64_t counter);
+uint64_t gbo_rng_u64(uint64_t seed, uint64_t stream, uint64_t counter);
 
 void gbo_update_batch(uint64_t log2_n, double a, double b, double c, uint64_t size,
                       uint64_t seed, uint32_t* out_pairs);
@@ -28,6 +29,9 @@ int gbo_pagerank(uint64_t n, const uint64_t* off, const uint32_t* nbr, double da
 void gbo_cc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* labels);
 int gbo_bc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, double* delta);
 uint64_t gbo_tc(uint64_t n, const uint64_t* off, const uint32_t* nbr);
+void gbo_kcore(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t* coreness);
+void gbo_coloring(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* colors);
+void gbo_mis(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t seed, uint8_t* in_set);
 
 void gbo_subset_to_dense(uint64_t n, const uint32_t* ids, uint64_t k, uint64_t* words);
 uint64_t gbo_subset_to_sparse(uint64_t n, const uint64_t* words, uint32_t* ids);

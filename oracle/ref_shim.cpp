@@ -14,6 +14,9 @@
 //   gbref_bfs_trace       gb::edge_map loop w/ mode_out (traversal.cpp:101-111)
 //   gbref_pagerank        gb::pagerank                 (algorithms.cpp:508-555)
 //   gbref_cc              gb::cc                       (algorithms.cpp:194-234)
+//   gbref_kcore           gb::kcore                    (algorithms.cpp:330-374)
+//   gbref_coloring        gb::coloring                 (algorithms.cpp:376-432)
+//   gbref_mis             gb::mis                      (algorithms.cpp:434-504)
 //   gbref_update_batch    gb::generate_update_batch    (batch.cpp:128-154)
 //   gbref_prepare_global  gb::prepare(GlobalSort)      (batch.cpp:30-42)
 //   gbref_chunked_*       registry "chunked_set" + apply_insert/apply_delete
@@ -270,6 +273,30 @@ int gbref_cc(void* csr, uint32_t* labels) {
     GraphView view(*static_cast<CsrGraph*>(csr));
     std::vector<VertexId> l = cc(view);
     std::memcpy(labels, l.data(), l.size() * sizeof(uint32_t));
+  });
+}
+
+int gbref_kcore(void* csr, uint64_t* out) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    std::vector<uint64_t> c = kcore(view);
+    std::memcpy(out, c.data(), c.size() * sizeof(uint64_t));
+  });
+}
+
+int gbref_coloring(void* csr, uint32_t* out) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    std::vector<uint32_t> c = coloring(view);
+    std::memcpy(out, c.data(), c.size() * sizeof(uint32_t));
+  });
+}
+
+int gbref_mis(void* csr, uint64_t seed, uint8_t* out) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    std::vector<uint8_t> s = mis(view, seed);
+    std::memcpy(out, s.data(), s.size());
   });
 }
 

@@ -122,4 +122,118 @@ void for_each_edge(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Op op
   GBG_LAUNCH(g, (for_each_edge_k<G, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, m, op);
 }
 
+// counts[u] += |{v in N(u) : pred(u, v)}| over the same balanced tiles.  A
+// warp's 32 consecutive edges cover a run of rows, so each row's hits are
+// summed with one match/ballot and added by one lane: a hub's tile costs a
+// handful of atomics instead of one per edge.
+template <class G, class Pred>
+__global__ void __launch_bounds__(kEdgeThreads) row_count_k(G g, const uint64_t* __restrict__ voff, uint64_t m,
+                                                             Pred pred, uint32_t* counts) {
+  __shared__ uint32_t s_row[kEdgeTile];
+  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kEdgeTile;
+  if (e0 >= m) return;
+  const uint32_t len = static_cast<uint32_t>(m - e0 < kEdgeTile ? m - e0 : kEdgeTile);
+  {
+    const uint32_t k0 = threadIdx.x * kEdgeIPT;
+    if (k0 < len) {
+      uint32_t r = row_of(voff, g.n, e0 + k0, 0);
+      uint64_t next = voff[r + 1];
+#pragma unroll
+      for (int j = 0; j < kEdgeIPT; ++j) {
+        if (k0 + j >= len) break;
+        if (next <= e0 + k0 + j) {
+          r = row_of(voff, g.n, e0 + k0 + j, r + 1);
+          next = voff[r + 1];
+        }
+        s_row[k0 + j] = r;
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b = 0; b < len; b += kEdgeThreads) {  // warp-uniform trip count
+    const uint32_t k = b + threadIdx.x;
+    const bool valid = k < len;
+    uint32_t u = 0xffffffffu;
+    bool hit = false;
+    if (valid) {
+      u = s_row[k];
+      const uint64_t e = e0 + k;
+      const uint32_t v = G::kContiguous ? g.at(e) : g.at(g.seg_begin(u) + (e - voff[u]));
+      hit = pred(u, v);
+    }
+    const uint32_t grp = __match_any_sync(0xffffffffu, u);
+    const uint32_t hits = __ballot_sync(0xffffffffu, hit) & grp;
+    if (valid && hits && lane == __ffs(grp) - 1) atomicAdd(counts + u, static_cast<uint32_t>(__popc(hits)));
+  }
+}
+
+// Filtered adjacency: for every arc (u, v) with pred(u, v), out[ooff[u] + k]
+// = v, k taken from cursor[u] (zeroed by the caller; ooff is the exclusive
+// scan of row_count's counts).  Same warp grouping as row_count: one atomic
+// per row run, positions by prefix popcount.  Order within a row is
+// unspecified.
+template <class G, class Pred>
+__global__ void __launch_bounds__(kEdgeThreads) row_compact_k(G g, const uint64_t* __restrict__ voff, uint64_t m,
+                                                               Pred pred, const uint64_t* __restrict__ ooff,
+                                                               uint32_t* cursor, uint32_t* out) {
+  __shared__ uint32_t s_row[kEdgeTile];
+  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kEdgeTile;
+  if (e0 >= m) return;
+  const uint32_t len = static_cast<uint32_t>(m - e0 < kEdgeTile ? m - e0 : kEdgeTile);
+  {
+    const uint32_t k0 = threadIdx.x * kEdgeIPT;
+    if (k0 < len) {
+      uint32_t r = row_of(voff, g.n, e0 + k0, 0);
+      uint64_t next = voff[r + 1];
+#pragma unroll
+      for (int j = 0; j < kEdgeIPT; ++j) {
+        if (k0 + j >= len) break;
+        if (next <= e0 + k0 + j) {
+          r = row_of(voff, g.n, e0 + k0 + j, r + 1);
+          next = voff[r + 1];
+        }
+        s_row[k0 + j] = r;
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b = 0; b < len; b += kEdgeThreads) {
+    const uint32_t k = b + threadIdx.x;
+    const bool valid = k < len;
+    uint32_t u = 0xffffffffu, v = 0;
+    bool hit = false;
+    if (valid) {
+      u = s_row[k];
+      const uint64_t e = e0 + k;
+      v = G::kContiguous ? g.at(e) : g.at(g.seg_begin(u) + (e - voff[u]));
+      hit = pred(u, v);
+    }
+    const uint32_t grp = __match_any_sync(0xffffffffu, u);
+    const uint32_t hits = __ballot_sync(0xffffffffu, hit) & grp;
+    const int leader = __ffs(grp) - 1;
+    uint32_t base = 0;
+    if (valid && hits && lane == leader) base = atomicAdd(cursor + u, static_cast<uint32_t>(__popc(hits)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) out[ooff[u] + base + __popc(hits & ((1u << lane) - 1))] = v;
+  }
+}
+
+template <class G, class Pred>
+void row_compact(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Pred pred, const uint64_t* ooff,
+                 uint32_t* cursor, uint32_t* out) {
+  if (m == 0) return;
+  const uint64_t tiles = (m + kEdgeTile - 1) / kEdgeTile;
+  GBG_LAUNCH(g, (row_compact_k<G, Pred>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, m, pred, ooff,
+             cursor, out);
+}
+
+template <class G, class Pred>
+void row_count(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Pred pred, uint32_t* counts) {
+  if (m == 0) return;
+  const uint64_t tiles = (m + kEdgeTile - 1) / kEdgeTile;
+  GBG_LAUNCH(g, (row_count_k<G, Pred>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, m, pred, counts);
+}
+
 }  // namespace gbg

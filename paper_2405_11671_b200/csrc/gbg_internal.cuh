@@ -226,6 +226,9 @@ void with_view(gbg_graph* g, F&& f) {
 // current; returns a pointer usable as CSR-like offsets for scheduling.
 const uint64_t* virtual_offsets(gbg_graph* g);
 
+// Every arc has its reverse (checked once per graph version, cc.cu).
+bool graph_is_symmetric(gbg_graph* g);
+
 // Optional phase timing (environment GBG_TRACE=1): CUDA events on the
 // handle's stream at named points, device-time deltas printed to stderr
 // when the tracer goes out of scope.

@@ -13,18 +13,9 @@
 #include <memory>
 
 #include "keys.cuh"
+#include "rng.cuh"
 
 namespace gbg {
-
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-  return x ^ (x >> 31);
-}
-__host__ __device__ __forceinline__ uint64_t hash_combine(uint64_t a, uint64_t b) {
-  return mix64(a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2)));
-}
 
 struct RmatParams {
   double t1, t2, t3;  // a, a+b, a+b+c

@@ -138,11 +138,23 @@ __device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, c
         if (dscan[mid] <= e) lo = mid; else hi = mid;
       }
       uint32_t i = lo;
-      uint64_t next = dscan[i + 1];
+      uint64_t next = i + 1 < nf ? dscan[i + 1] : E;
 #pragma unroll
       for (int j = 0; j < kPushIPT; ++j) {
         if (k0 + j >= len) break;
-        while (next <= e + j) next = dscan[++i + 1];
+        while (next <= e + j) {
+          ++i;
+          next = i + 1 < nf ? dscan[i + 1] : E;
+          if (next <= e + j) {  // a run of empty / short segments: search it instead of walking it
+            uint32_t l2 = i + 1, h2 = nf;  // dscan[l2] <= e + j < dscan[h2]
+            while (h2 - l2 > 1) {
+              const uint32_t mid = (l2 + h2) >> 1;
+              if (dscan[mid] <= e + j) l2 = mid; else h2 = mid;
+            }
+            i = l2;
+            next = i + 1 < nf ? dscan[i + 1] : E;
+          }
+        }
         s_idx[k0 + j] = i;
       }
     }
@@ -189,6 +201,42 @@ __global__ void __launch_bounds__(kPushThreads)
            uint32_t* __restrict__ out_bm, unsigned long long* packed) {
   __shared__ uint32_t s_idx[kPushTile];
   push_tile(g, F, nf, dscan, E, op, out, out_dscan, out_bm, packed, blockIdx.x, s_idx);
+}
+
+// one push over a frontier list with its degree prefix (E = total degree)
+template <class G, class Op>
+inline void push_list(gbg_graph* g, G view, const uint32_t* F, uint64_t nf, const uint64_t* dscan, uint64_t E, Op op,
+                      uint32_t* out, uint64_t* out_dscan, unsigned long long* packed) {
+  if (!nf || !E) return;
+  const uint64_t tiles = (E + kPushTile - 1) / kPushTile;
+  GBG_LAUNCH(g, (push_k<G, Op>), static_cast<unsigned>(tiles), kPushThreads, 0, view, F, static_cast<uint32_t>(nf),
+             dscan, E, op, out, out_dscan, nullptr, packed);
+}
+
+// Select the vertices with pred(v) into an ascending-by-warp id list with
+// its degree prefix (packed counter, as push_tile emits).
+template <class G, class Pred>
+__global__ void select_k(G g, Pred pred, uint32_t* list, uint64_t* dscan, unsigned long long* packed) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < g.n; base += stride) {
+    const uint64_t v = base + threadIdx.x;
+    const bool take = v < g.n && pred(static_cast<uint32_t>(v));
+    const uint32_t mask = __ballot_sync(0xffffffffu, take);
+    if (!mask) continue;
+    const uint64_t dv = take ? g.degree(static_cast<uint32_t>(v)) : 0;
+    const uint64_t dinc = warp_inclusive_scan(dv);
+    const uint64_t dtot = __shfl_sync(0xffffffffu, dinc, 31);
+    const int leader = __ffs(mask) - 1;
+    unsigned long long old = 0;
+    if (lane == leader) old = atomicAdd(packed, (static_cast<unsigned long long>(__popc(mask)) << kPackShift) | dtot);
+    old = __shfl_sync(0xffffffffu, old, leader);
+    if (take) {
+      const uint64_t pos = pack_count(old) + __popc(mask & ((1u << lane) - 1));
+      list[pos] = static_cast<uint32_t>(v);
+      dscan[pos] = pack_degsum(old) + dinc - dv;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- pull

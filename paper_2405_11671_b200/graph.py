@@ -153,6 +153,9 @@ _SIGS = {
     "gbg_pagerank_prepare": [_vp, _f64p],
     "gbg_bc": [_vp, C.c_uint32, _f64p],
     "gbg_bc_device": [_vp, C.c_uint32, _vp],
+    "gbg_kcore": [_vp, _u64p],
+    "gbg_coloring": [_vp, _u32p],
+    "gbg_mis": [_vp, C.c_uint64, _u8p],
     "gbg_load_gbcsr1": [C.c_char_p, C.c_int, _gpp],
     "gbg_save_gbcsr1": [_vp, C.c_char_p],
 }
@@ -452,6 +455,30 @@ def cc(g: _Graph) -> np.ndarray:
 
 def cc_device(g: _Graph, out_ptr: int):
     _check(_L.gbg_cc_device(g.handle, out_ptr))
+
+
+def kcore(g: _Graph) -> np.ndarray:
+    """gb::kcore (algorithms.cpp:330-374): coreness per vertex (uint64)."""
+    out = np.empty(g.num_vertices(), dtype=np.uint64)
+    _check(_L.gbg_kcore(g.handle, _p(out, _u64p)))
+    return out
+
+
+def coloring(g: _Graph) -> np.ndarray:
+    """gb::coloring (algorithms.cpp:376-432): first-fit colours in
+    largest-log-degree-first order (uint32).  Symmetric graphs only."""
+    out = np.empty(g.num_vertices(), dtype=np.uint32)
+    _check(_L.gbg_coloring(g.handle, _p(out, _u32p)))
+    return out
+
+
+def mis(g: _Graph, seed: int = 1) -> np.ndarray:
+    """gb::mis (algorithms.cpp:434-504): 0/1 membership (uint8) of the
+    lexicographically-first MIS under (rng_u64(seed, 7, v), v).  Symmetric
+    graphs only."""
+    out = np.empty(g.num_vertices(), dtype=np.uint8)
+    _check(_L.gbg_mis(g.handle, seed, _p(out, _u8p)))
+    return out
 
 
 def triangle_count(g: _Graph) -> int:

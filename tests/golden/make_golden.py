@@ -16,6 +16,13 @@ Per scale S (R-MAT a=.57 b=c=.19, arcs = 16*2^S, seed 1):
   tc         triangle count from the C restatement (the reference has none)
 At S=22 also the config-5 update sequence on the reference "chunked_set"
 container (see `updates()`).
+
+    python tests/golden/make_golden.py --greedy 16 20 24
+
+adds (in place) the priority-order consumers of §8(f) row 3:
+  kcore      digest(uint64 coreness), max coreness
+  coloring   digest(uint32 colours), colour count
+  mis        seed 1 (AlgoParams default): digest(uint8 flags), set size
 """
 import json
 import os
@@ -138,5 +145,32 @@ def main(scales):
         print(f"s{S}: written", flush=True)
 
 
+def greedy(scales):
+    ref = Ref()
+    for S in scales:
+        n, off, nbr = graph(ref, S)
+        path = os.path.join(HERE, f"rmat_s{S}.json")
+        with open(path) as f:
+            rec = json.load(f)
+        g = ref.csr(n, off, nbr)
+        t = time.time()
+        core = g.kcore()
+        rec["kcore"] = dict(digest=digest(core), max_core=int(core.max()))
+        print(f"s{S}: kcore {time.time() - t:.1f}s {rec['kcore']}", flush=True)
+        t = time.time()
+        col = g.coloring()
+        rec["coloring"] = dict(digest=digest(col), colors=int(col.max()) + 1)
+        print(f"s{S}: coloring {time.time() - t:.1f}s {rec['coloring']}", flush=True)
+        t = time.time()
+        flags = g.mis(1)
+        rec["mis"] = dict(seed=1, digest=digest(flags), size=int(flags.sum()))
+        print(f"s{S}: mis {time.time() - t:.1f}s {rec['mis']}", flush=True)
+        with open(path, "w") as f:
+            json.dump(rec, f, indent=1)
+
+
 if __name__ == "__main__":
-    main([int(x) for x in sys.argv[1:]] or [16, 20])
+    if sys.argv[1:2] == ["--greedy"]:
+        greedy([int(x) for x in sys.argv[2:]])
+    else:
+        main([int(x) for x in sys.argv[1:]] or [16, 20])

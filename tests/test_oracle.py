@@ -322,3 +322,112 @@ def test_set_apply_matches_chunked_set(ref, orc):
     k2, o3, n3 = orc.set_apply(n, o2, n2, orc.prepare_global(batch), False)
     assert k2 == dele == ins
     assert np.array_equal(o3, off) and np.array_equal(n3, nbr)
+
+
+# ------------------------------------------- priority-order consumers (§8f)
+def _directed(n, p, seed):
+    """Sorted unique arcs without self-loops, no reverse pairing."""
+    rng = np.random.default_rng(seed)
+    a = rng.random((n, n)) < p
+    np.fill_diagonal(a, False)
+    s, d = np.nonzero(a)
+    return np.stack([s, d], axis=1).astype(np.uint32)
+
+
+def _check_coloring(n, pairs, colors):
+    """checks.cpp:42-58"""
+    deg = np.bincount(pairs[:, 0], minlength=n) if len(pairs) else np.zeros(n, np.int64)
+    assert not np.any(colors[pairs[:, 0]] == colors[pairs[:, 1]])
+    assert colors.max(initial=0) <= deg.max(initial=0)
+
+
+def _check_mis(n, off, nbr, flags):
+    """checks.cpp:60-81"""
+    src = np.repeat(np.arange(n), np.diff(off.astype(np.int64)))
+    assert not np.any(flags[src] & flags[nbr])
+    covered = flags.astype(bool).copy()
+    covered[src[flags[nbr] == 1]] = True
+    assert covered.all()
+
+
+def test_kcore_known_answers(ref, orc):
+    # test_algorithms.cpp:228-241
+    off, nbr = csr(4, T4_PAIRS)
+    assert orc.kcore(4, off, nbr).tolist() == ref.csr(4, off, nbr).kcore().tolist() == [2, 2, 2, 1]
+    n, pairs = undirected(7, [(0, 1), (0, 2), (1, 3), (1, 4), (2, 5), (2, 6)], orc)
+    assert orc.kcore(n, *csr(n, pairs)).tolist() == [1] * 7
+    for k in (4, 9):
+        n, pairs = undirected(k, complete(k), orc)
+        assert orc.kcore(n, *csr(n, pairs)).tolist() == [k - 1] * k
+    off, nbr = csr(5, np.zeros((0, 2), np.uint32))
+    assert orc.kcore(5, off, nbr).tolist() == [0] * 5
+
+
+def test_kcore_matches_reference(ref, orc):
+    # test_algorithms.cpp:243-250 (seeded graphs) plus directed inputs: the
+    # out-degree peel is order-independent there too
+    for trial in range(15):
+        n, pairs = ref.er(200, 0.03, 1700 + trial)
+        off, nbr = csr(n, pairs)
+        assert np.array_equal(orc.kcore(n, off, nbr), ref.csr(n, off, nbr).kcore())
+    for trial in range(5):
+        pairs = _directed(120, 0.05, trial)
+        off, nbr = csr(120, pairs)
+        assert np.array_equal(orc.kcore(120, off, nbr), ref.csr(120, off, nbr).kcore())
+    n, pairs = ref.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    assert np.array_equal(orc.kcore(n, off, nbr), ref.csr(n, off, nbr).kcore())
+
+
+def test_coloring_matches_reference(ref, orc):
+    # test_algorithms.cpp:252-264
+    off, nbr = csr(5, np.zeros((0, 2), np.uint32))
+    assert orc.coloring(5, off, nbr).tolist() == ref.csr(5, off, nbr).coloring().tolist() == [0] * 5
+    for trial in range(20):
+        n, pairs = ref.er(120, 0.06, 1900 + trial)
+        off, nbr = csr(n, pairs)
+        c = orc.coloring(n, off, nbr)
+        assert np.array_equal(c, ref.csr(n, off, nbr).coloring())
+        _check_coloring(n, pairs, c)
+    n, pairs = ref.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    c = orc.coloring(n, off, nbr)
+    assert np.array_equal(c, ref.csr(n, off, nbr).coloring())
+    _check_coloring(n, pairs, c)
+
+
+def test_mis_matches_reference(ref, orc):
+    # test_algorithms.cpp:266-292
+    off, nbr = csr(4, T4_PAIRS)
+    f = orc.mis(4, off, nbr, 3)
+    assert np.array_equal(f, ref.csr(4, off, nbr).mis(3))
+    assert (f.sum() == 1 and f[2]) or (f.sum() == 2 and f[3])
+    off, nbr = csr(4, np.zeros((0, 2), np.uint32))
+    assert orc.mis(4, off, nbr, 1).tolist() == [1, 1, 1, 1]
+    for trial in range(50):
+        n, pairs = ref.er(150, 0.05, 2100 + trial)
+        off, nbr = csr(n, pairs)
+        f = orc.mis(n, off, nbr, trial)
+        assert np.array_equal(f, ref.csr(n, off, nbr).mis(trial))
+        _check_mis(n, off, nbr, f)
+    n, pairs = ref.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    f = orc.mis(n, off, nbr, 1)
+    assert np.array_equal(f, ref.csr(n, off, nbr).mis(1))
+    _check_mis(n, off, nbr, f)
+
+
+def test_mis_is_lexicographically_first(orc):
+    """The rounds give the sequential greedy MIS in (rank, id) order."""
+    for trial in range(10):
+        n, pairs = undirected(60, [tuple(e) for e in _directed(60, 0.1, 50 + trial)], orc)
+        off, nbr = csr(n, pairs)
+        f = orc.mis(n, off, nbr, trial)
+        rank = [orc.rng_u64(trial, 7, v) for v in range(n)]
+        chosen = np.zeros(n, np.uint8)
+        blocked = np.zeros(n, bool)
+        for v in sorted(range(n), key=lambda v: (rank[v], v)):
+            if not blocked[v]:
+                chosen[v] = 1
+                blocked[nbr[off[v]:off[v + 1]]] = True
+        assert np.array_equal(f, chosen)
