@@ -9,7 +9,7 @@
 // Reads served to CPU callers (map_neighbors & co.) come from a host mirror
 // of the adjacency, fetched once from the device (gbg_export_csr) and
 // refreshed after every update; the device algorithms (gbg::bfs, pagerank,
-// cc, triangle_count below) run on the device copy.  Errors come back as the
+// cc, bc, kcore, coloring, mis, triangle_count below) run on the device copy.  Errors come back as the
 // reference's exception types.
 //
 // Header-only; needs the reference include tree (-I <reference>/include) and
@@ -229,6 +229,27 @@ inline std::vector<double> bc(const GpuGraph& g, gb::VertexId source) {
   return d;
 }
 
+// gb::kcore (algorithms.cpp:330-374)
+inline std::vector<uint64_t> kcore(const GpuGraph& g) {
+  std::vector<uint64_t> c(g.num_vertices());
+  check(gbg_kcore(g.handle(), c.data()));
+  return c;
+}
+
+// gb::coloring (algorithms.cpp:376-432); symmetric graphs
+inline std::vector<uint32_t> coloring(const GpuGraph& g) {
+  std::vector<uint32_t> c(g.num_vertices());
+  check(gbg_coloring(g.handle(), c.data()));
+  return c;
+}
+
+// gb::mis (algorithms.cpp:434-504); symmetric graphs
+inline std::vector<uint8_t> mis(const GpuGraph& g, uint64_t seed) {
+  std::vector<uint8_t> f(g.num_vertices());
+  check(gbg_mis(g.handle(), seed, f.data()));
+  return f;
+}
+
 inline uint64_t triangle_count(const GpuGraph& g) {
   uint64_t t = 0;
   check(gbg_tc(g.handle(), &t));
@@ -255,6 +276,24 @@ inline const std::vector<gb::AlgorithmInfo>& gpu_algorithms() {
        [](const gb::GraphView& v, const gb::AlgoParams&) {
          gb::CanonicalOutput out;
          for (gb::VertexId l : cc(device_of(v))) out.ints.push_back(l);
+         return out;
+       }},
+      {"kcore",
+       [](const gb::GraphView& v, const gb::AlgoParams&) {
+         gb::CanonicalOutput out;
+         out.ints = kcore(device_of(v));
+         return out;
+       }},
+      {"coloring",
+       [](const gb::GraphView& v, const gb::AlgoParams&) {
+         gb::CanonicalOutput out;
+         for (uint32_t c : coloring(device_of(v))) out.ints.push_back(c);
+         return out;
+       }},
+      {"mis",
+       [](const gb::GraphView& v, const gb::AlgoParams& p) {
+         gb::CanonicalOutput out;
+         for (uint8_t f : mis(device_of(v), p.seed)) out.ints.push_back(f);
          return out;
        }},
       {"pagerank",
