@@ -444,7 +444,10 @@ def main():
         # back to host memory inside the timed call)
         for name, fn, summary in (("kcore", lambda: gbg.kcore(g), lambda o: {"max_core": int(o.max())}),
                                   ("coloring", lambda: gbg.coloring(g), lambda o: {"colors": int(o.max()) + 1}),
-                                  ("mis", lambda: gbg.mis(g, 1), lambda o: {"size": int(o.sum())})):
+                                  ("mis", lambda: gbg.mis(g, 1), lambda o: {"size": int(o.sum())}),
+                                  ("ldd", lambda: gbg.ldd(g, 0.2, 1),
+                                   lambda o: {"clusters": int((o[0] == np.arange(o[0].size)).sum()),
+                                              "rounds": int(o[2].max()) + 1})):
             t_alg, out = host_time(fn, max(1, min(args.steps, 3)), 1)
             workloads[f"{name}_s{S}"] = {"ms": t_alg * 1e3, "arcs_per_s": m / t_alg, **summary(out)}
             log(f"{name}_s{S}: {t_alg * 1e3:.1f} ms")

@@ -9,7 +9,7 @@
 // Reads served to CPU callers (map_neighbors & co.) come from a host mirror
 // of the adjacency, fetched once from the device (gbg_export_csr) and
 // refreshed after every update; the device algorithms (gbg::bfs, pagerank,
-// cc, bc, kcore, coloring, mis, triangle_count below) run on the device copy.  Errors come back as the
+// cc, bc, ldd, kcore, coloring, mis, triangle_count below) run on the device copy.  Errors come back as the
 // reference's exception types.
 //
 // Header-only; needs the reference include tree (-I <reference>/include) and
@@ -250,6 +250,17 @@ inline std::vector<uint8_t> mis(const GpuGraph& g, uint64_t seed) {
   return f;
 }
 
+// gb::ldd (algorithms.cpp:114-188), the reference's result struct
+inline gb::LddResult ldd(const GpuGraph& g, double beta, uint64_t seed) {
+  gb::LddResult r;
+  const uint64_t n = g.num_vertices();
+  r.labels.resize(n);
+  r.parents.resize(n);
+  r.rounds.resize(n);
+  check(gbg_ldd(g.handle(), beta, seed, r.labels.data(), r.parents.data(), r.rounds.data()));
+  return r;
+}
+
 inline uint64_t triangle_count(const GpuGraph& g) {
   uint64_t t = 0;
   check(gbg_tc(g.handle(), &t));
@@ -276,6 +287,12 @@ inline const std::vector<gb::AlgorithmInfo>& gpu_algorithms() {
        [](const gb::GraphView& v, const gb::AlgoParams&) {
          gb::CanonicalOutput out;
          for (gb::VertexId l : cc(device_of(v))) out.ints.push_back(l);
+         return out;
+       }},
+      {"ldd",
+       [](const gb::GraphView& v, const gb::AlgoParams& p) {
+         gb::CanonicalOutput out;
+         for (gb::VertexId l : ldd(device_of(v), p.beta, p.seed).labels) out.ints.push_back(l);
          return out;
        }},
       {"kcore",

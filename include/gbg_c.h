@@ -190,6 +190,14 @@ gbg_status gbg_coloring(gbg_graph* g, uint32_t* colors);
 /* gb::mis (algorithms.cpp:434-504): in_set[n] 0/1, the lexicographically
  * first MIS under (rng_u64(seed, 7, v), v).  Symmetric graphs only. */
 gbg_status gbg_mis(gbg_graph* g, uint64_t seed, uint8_t* in_set);
+/* gb::ldd (algorithms.cpp:114-188): labels[n] (cluster centre), parents[n]
+ * (tree edge; itself at centres; UINT32_MAX when none), rounds[n] (round
+ * joined).  parents / rounds may be NULL.  beta outside (0, 1] ->
+ * GBG_ERR_INVALID_ARGUMENT (std::invalid_argument). */
+gbg_status gbg_ldd(gbg_graph* g, double beta, uint64_t seed, uint32_t* labels, uint32_t* parents, uint64_t* rounds);
+/* Test hook: the device log1p behind ldd's Exponential shifts on n host
+ * values (must equal the host C library's log1p bit for bit). */
+gbg_status gbg_selftest_log1p(const double* x, uint64_t n, double* out);
 /* Triangle count (not in the reference): orient u->v iff
  * (deg u, u) < (deg v, v) (derive_filter, derive.hpp:48-61), count
  * |N+(u) ∩ N+(v)| over oriented arcs. */

@@ -151,6 +151,15 @@ class Ref:
     def hash_combine(self, a: int, b: int) -> int:
         return self.L.gbref_hash_combine(a, b)
 
+    def log1p(self, x):
+        """std::log1p as the reference's C library computes it (rng.hpp:33)."""
+        self.L.gbref_log1p.argtypes = [_f64p, C.c_uint64, _f64p]
+        self.L.gbref_log1p.restype = None
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self.L.gbref_log1p(ptr(x, _f64p), x.size, ptr(out, _f64p))
+        return out
+
     # graphs -> (n, pairs[m,2] u32)
     def _take_graph(self, h):
         if not h:
@@ -296,6 +305,16 @@ class RefCsr:
         out = np.empty(self.n, dtype=np.uint8)
         self.ref._check(L.gbref_mis(self.h, seed, ptr(out, _u8p)))
         return out
+
+    def ldd(self, beta=0.2, seed=1):
+        """gb::ldd (algorithms.cpp:114-188) -> (labels, parents, rounds)."""
+        L = self.ref.L
+        L.gbref_ldd.argtypes = [C.c_void_p, C.c_double, C.c_uint64, _u32p, _u32p, _u64p]
+        lab = np.empty(self.n, dtype=np.uint32)
+        par = np.empty(self.n, dtype=np.uint32)
+        rnd = np.empty(self.n, dtype=np.uint64)
+        self.ref._check(L.gbref_ldd(self.h, beta, seed, ptr(lab, _u32p), ptr(par, _u32p), ptr(rnd, _u64p)))
+        return lab, par, rnd
 
     def edge_map(self, ids, cond_mask, mode, early_exit=True):
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
@@ -455,6 +474,15 @@ class Oracle:
     def _csr_args(self, off, nbr):
         return (ptr(np.ascontiguousarray(off, dtype=np.uint64), _u64p),
                 ptr(np.ascontiguousarray(nbr, dtype=np.uint32), _u32p))
+
+    def ldd(self, n, off, nbr, beta=0.2, seed=1):
+        self.L.gbo_ldd.argtypes = [C.c_uint64, _u64p, _u32p, C.c_double, C.c_uint64, _u32p, _u32p, _u64p]
+        lab = np.empty(max(n, 1), dtype=np.uint32)
+        par = np.empty(max(n, 1), dtype=np.uint32)
+        rnd = np.empty(max(n, 1), dtype=np.uint64)
+        if self.L.gbo_ldd(n, *self._csr_args(off, nbr), beta, seed, ptr(lab, _u32p), ptr(par, _u32p), ptr(rnd, _u64p)):
+            raise ValueError("ldd: beta must be in (0, 1]")
+        return lab[:n], par[:n], rnd[:n]
 
     def kcore(self, n, off, nbr):
         self.L.gbo_kcore.argtypes = [C.c_uint64, _u64p, _u32p, _u64p]

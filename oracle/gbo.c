@@ -647,3 +647,68 @@ void gbo_mis(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t seed
   free(decided);
   free(rel);
 }
+
+/* algorithms.cpp:114-188: shifts Exponential(beta) from rng_exponential
+ * (rng.hpp:31-35, the C library's log1p), start = floor(max_shift - shift);
+ * synchronous rounds: arrivals (min centre over the previous round's
+ * joiners), self-starts, labelling, then each joiner's parent = smallest
+ * same-cluster neighbour from an earlier round (itself at centres).
+ * Returns 1 (invalid argument) unless 0 < beta <= 1. */
+int gbo_ldd(uint64_t n, const uint64_t* off, const uint32_t* nbr, double beta, uint64_t seed, uint32_t* label,
+            uint32_t* parent, uint64_t* rounds) {
+  if (!(beta > 0.0 && beta <= 1.0)) return 1;
+  if (!n) return 0;
+  const uint32_t none = UINT32_MAX;
+  double* shift = (double*)malloc(n * sizeof(double));
+  uint64_t* start = (uint64_t*)malloc(n * sizeof(uint64_t));
+  uint32_t* cand = (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* front = (uint32_t*)malloc(n * sizeof(uint32_t));
+  uint32_t* next = (uint32_t*)malloc(n * sizeof(uint32_t));
+  double max_shift = 0.0;
+  for (uint64_t v = 0; v < n; ++v) {
+    shift[v] = -log1p(-gbo_rng_double(seed, v, 0)) / beta;
+    if (shift[v] > max_shift) max_shift = shift[v];
+  }
+  for (uint64_t v = 0; v < n; ++v) {
+    start[v] = (uint64_t)floor(max_shift - shift[v]);
+    label[v] = cand[v] = parent[v] = none;
+    rounds[v] = 0;
+  }
+  uint64_t labeled = 0, nf = 0, round = 0;
+  while (labeled < n) {
+    for (uint64_t i = 0; i < nf; ++i) {
+      uint32_t u = front[i], c = label[u];
+      for (uint64_t e = off[u]; e < off[u + 1]; ++e)
+        if (label[nbr[e]] == none && c < cand[nbr[e]]) cand[nbr[e]] = c;
+    }
+    for (uint64_t v = 0; v < n; ++v)
+      if (label[v] == none && start[v] <= round && (uint32_t)v < cand[v]) cand[v] = (uint32_t)v;
+    uint64_t nn = 0;
+    for (uint64_t v = 0; v < n; ++v) {
+      if (label[v] != none || cand[v] == none) continue;
+      label[v] = cand[v];
+      rounds[v] = round;
+      next[nn++] = (uint32_t)v;
+    }
+    for (uint64_t i = 0; i < nn; ++i) {
+      uint32_t v = next[i], c = label[v], best = none;
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+        uint32_t u = nbr[e];
+        if (label[u] == c && rounds[u] < rounds[v] && u < best) best = u;
+      }
+      parent[v] = (v == c && best == none) ? v : best;
+    }
+    labeled += nn;
+    uint32_t* t = front;
+    front = next;
+    next = t;
+    nf = nn;
+    ++round;
+  }
+  free(shift);
+  free(start);
+  free(cand);
+  free(front);
+  free(next);
+  return 0;
+}

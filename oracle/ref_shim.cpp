@@ -17,6 +17,8 @@
 //   gbref_kcore           gb::kcore                    (algorithms.cpp:330-374)
 //   gbref_coloring        gb::coloring                 (algorithms.cpp:376-432)
 //   gbref_mis             gb::mis                      (algorithms.cpp:434-504)
+//   gbref_ldd             gb::ldd                      (algorithms.cpp:114-188)
+//   gbref_log1p           std::log1p of the reference's C library (rng.hpp:33)
 //   gbref_update_batch    gb::generate_update_batch    (batch.cpp:128-154)
 //   gbref_prepare_global  gb::prepare(GlobalSort)      (batch.cpp:30-42)
 //   gbref_chunked_*       registry "chunked_set" + apply_insert/apply_delete
@@ -29,6 +31,7 @@
 // gbref_last_error().
 
 #include <atomic>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <limits>
@@ -298,6 +301,20 @@ int gbref_mis(void* csr, uint64_t seed, uint8_t* out) {
     std::vector<uint8_t> s = mis(view, seed);
     std::memcpy(out, s.data(), s.size());
   });
+}
+
+int gbref_ldd(void* csr, double beta, uint64_t seed, uint32_t* labels, uint32_t* parents, uint64_t* rounds) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    LddResult r = ldd(view, beta, seed);
+    std::memcpy(labels, r.labels.data(), r.labels.size() * sizeof(uint32_t));
+    std::memcpy(parents, r.parents.data(), r.parents.size() * sizeof(uint32_t));
+    std::memcpy(rounds, r.rounds.data(), r.rounds.size() * sizeof(uint64_t));
+  });
+}
+
+void gbref_log1p(const double* x, uint64_t n, double* out) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = std::log1p(x[i]);
 }
 
 // One edge_map call with a membership cond given as a byte mask (cond[v] !=

@@ -156,6 +156,8 @@ _SIGS = {
     "gbg_kcore": [_vp, _u64p],
     "gbg_coloring": [_vp, _u32p],
     "gbg_mis": [_vp, C.c_uint64, _u8p],
+    "gbg_ldd": [_vp, C.c_double, C.c_uint64, _u32p, _u32p, _u64p],
+    "gbg_selftest_log1p": [_f64p, C.c_uint64, _f64p],
     "gbg_load_gbcsr1": [C.c_char_p, C.c_int, _gpp],
     "gbg_save_gbcsr1": [_vp, C.c_char_p],
 }
@@ -478,6 +480,25 @@ def mis(g: _Graph, seed: int = 1) -> np.ndarray:
     graphs only."""
     out = np.empty(g.num_vertices(), dtype=np.uint8)
     _check(_L.gbg_mis(g.handle, seed, _p(out, _u8p)))
+    return out
+
+
+def ldd(g: _Graph, beta: float = 0.2, seed: int = 1):
+    """gb::ldd (algorithms.cpp:114-188) -> (labels u32, parents u32,
+    rounds u64); UINT32_MAX marks no parent."""
+    n = g.num_vertices()
+    labels = np.empty(n, dtype=np.uint32)
+    parents = np.empty(n, dtype=np.uint32)
+    rounds = np.empty(n, dtype=np.uint64)
+    _check(_L.gbg_ldd(g.handle, beta, seed, _p(labels, _u32p), _p(parents, _u32p), _p(rounds, _u64p)))
+    return labels, parents, rounds
+
+
+def selftest_log1p(x) -> np.ndarray:
+    """The device log1p used for ldd's shifts, on host values (test hook)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _check(_L.gbg_selftest_log1p(_p(x, _f64p), x.size, _p(out, _f64p)))
     return out
 
 

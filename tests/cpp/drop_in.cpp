@@ -11,7 +11,7 @@
 //   - static containers reject updates, CsrGraph::build errors
 //     (test_containers.cpp:26-52)
 //   - all containers agree on degrees and neighbour lists (test_containers.cpp:147-165)
-//   - device bfs / cc / bc / kcore / coloring / mis / pagerank against the
+//   - device bfs / cc / bc / ldd / kcore / coloring / mis / pagerank against the
 //     gb:: functions, and the AlgorithmInfo entries against the registry
 // Prints one PASS/FAIL line per check; exit status = number of failures.
 #include <algorithm>
@@ -174,7 +174,7 @@ int main() {
     return true;
   });
 
-  check("device bfs / cc / bc / kcore / coloring / mis / pagerank match gb:: on seeded graphs", [&](std::string& d) {
+  check("device bfs / cc / bc / ldd / kcore / coloring / mis / pagerank match gb:: on seeded graphs", [&](std::string& d) {
     for (int trial = 0; trial < 20; ++trial) {
       GraphData g = generate_er({150, 0.03}, 100 + trial);
       CsrGraph cpu = CsrGraph::build(g.n, g.arcs);
@@ -189,6 +189,8 @@ int main() {
         for (size_t v = 0; v < bd.size(); ++v)  // the reference's own bc bar (bench.cpp:234-241)
           if (std::abs(bd[v] - bw[v]) > 1e-9) return d = "bc at " + std::to_string(v), false;
         if (gbg::kcore(dev) != kcore(cv)) return d = "kcore", false;
+        LddResult la = gbg::ldd(dev, 0.2, trial), lb = ldd(cv, 0.2, trial);
+        if (la.labels != lb.labels || la.parents != lb.parents || la.rounds != lb.rounds) return d = "ldd", false;
         if (gbg::coloring(dev) != coloring(cv)) return d = "coloring", false;
         if (gbg::mis(dev, trial) != mis(cv, trial)) return d = "mis", false;
         auto a = gbg::pagerank(dev, 0.85, 20, 1e-4);

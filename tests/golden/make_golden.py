@@ -23,6 +23,8 @@ adds (in place) the priority-order consumers of §8(f) row 3:
   kcore      digest(uint64 coreness), max coreness
   coloring   digest(uint32 colours), colour count
   mis        seed 1 (AlgoParams default): digest(uint8 flags), set size
+  ldd        beta 0.2, seed 1 (AlgoParams defaults): digests of labels,
+             parents, rounds; cluster count, last round
 """
 import json
 import os
@@ -165,6 +167,12 @@ def greedy(scales):
         flags = g.mis(1)
         rec["mis"] = dict(seed=1, digest=digest(flags), size=int(flags.sum()))
         print(f"s{S}: mis {time.time() - t:.1f}s {rec['mis']}", flush=True)
+        t = time.time()
+        lab, par, rnd = g.ldd(0.2, 1)
+        rec["ldd"] = dict(beta=0.2, seed=1, labels_digest=digest(lab), parents_digest=digest(par),
+                          rounds_digest=digest(rnd), clusters=int((lab == np.arange(n)).sum()),
+                          last_round=int(rnd.max()))
+        print(f"s{S}: ldd {time.time() - t:.1f}s {rec['ldd']}", flush=True)
         with open(path, "w") as f:
             json.dump(rec, f, indent=1)
 

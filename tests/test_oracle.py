@@ -5,7 +5,7 @@ the golden fixtures.  No GPU needed."""
 import numpy as np
 import pytest
 
-from oracle.bindings import digest, max_degree_source
+from oracle.bindings import RefError, digest, max_degree_source
 from tests.conftest import golden
 from tests.helpers import T4_PAIRS, complete, csr, members, star, undirected
 
@@ -431,3 +431,46 @@ def test_mis_is_lexicographically_first(orc):
                 chosen[v] = 1
                 blocked[nbr[off[v]:off[v + 1]]] = True
         assert np.array_equal(f, chosen)
+
+
+def _check_ldd(n, off, nbr, labels):
+    """checks.cpp:83-117: every vertex labelled, centres in their own
+    cluster, clusters connected through same-cluster arcs."""
+    assert (labels < n).all()
+    assert (labels[labels] == labels).all()
+    reached = labels == np.arange(n)
+    stack = list(np.nonzero(reached)[0])
+    while stack:
+        u = stack.pop()
+        for v in nbr[off[u]:off[u + 1]]:
+            if not reached[v] and labels[v] == labels[u]:
+                reached[v] = True
+                stack.append(v)
+    assert reached.all()
+
+
+def test_ldd_matches_reference(ref, orc):
+    # test_algorithms.cpp:90-104 (partition per trial, beta range) + exact outputs
+    off, nbr = csr(4, T4_PAIRS)
+    for bad in (0.0, 1.5, -1.0):
+        with pytest.raises(ValueError):
+            orc.ldd(4, off, nbr, bad, 1)
+        with pytest.raises(RefError, match="reference error 2"):  # std::invalid_argument
+            ref.csr(4, off, nbr).ldd(bad, 1)
+    for trial in range(20):
+        n, pairs = ref.er(150, 0.03, 700 + trial)
+        off, nbr = csr(n, pairs)
+        beta = (0.05, 0.2, 0.5, 1.0)[trial % 4]
+        got = orc.ldd(n, off, nbr, beta, trial)
+        want = ref.csr(n, off, nbr).ldd(beta, trial)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b), trial
+        _check_ldd(n, off, nbr, got[0])
+    pairs = _directed(100, 0.04, 3)  # directed: parents may be missing, still exact
+    off, nbr = csr(100, pairs)
+    for a, b in zip(orc.ldd(100, off, nbr, 0.3, 5), ref.csr(100, off, nbr).ldd(0.3, 5)):
+        assert np.array_equal(a, b)
+    n, pairs = ref.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    for a, b in zip(orc.ldd(n, off, nbr, 0.2, 1), ref.csr(n, off, nbr).ldd(0.2, 1)):
+        assert np.array_equal(a, b)
