@@ -182,6 +182,22 @@ class GpuBlockedGraph final : public GpuGraph {
   }
 };
 
+// gb::CompressedCsrGraph (compressed_csr.hpp:12-46) on the device; static,
+// no parallel maps (its capabilities say so, like the reference's).
+class GpuCompressedGraph final : public GpuGraph {
+ public:
+  using GpuGraph::GpuGraph;
+  static std::unique_ptr<GpuCompressedGraph> build(uint64_t n, std::span<const gb::Edge> arcs) {
+    gbg_graph* csr = nullptr;
+    check(gbg_csr_from_arcs(n, reinterpret_cast<const uint32_t*>(arcs.data()), arcs.size(), &csr));
+    gbg_graph* h = nullptr;
+    const gbg_status st = gbg_compressed_from(csr, &h);
+    gbg_graph_destroy(csr);
+    check(st);
+    return std::make_unique<GpuCompressedGraph>(h);
+  }
+};
+
 // Factories in the shape of the reference registry (registry.cpp:112-142),
 // for VerifyOptions::extra_containers.
 inline const std::vector<gb::ContainerInfo>& gpu_containers() {
@@ -190,6 +206,8 @@ inline const std::vector<gb::ContainerInfo>& gpu_containers() {
        [](const gb::GraphData& g) -> gb::GraphContainerPtr { return GpuCsrGraph::build(g.n, g.arcs); }},
       {"gpu_blocked", true,
        [](const gb::GraphData& g) -> gb::GraphContainerPtr { return GpuBlockedGraph::build(g.n, g.arcs); }},
+      {"gpu_compressed", false,
+       [](const gb::GraphData& g) -> gb::GraphContainerPtr { return GpuCompressedGraph::build(g.n, g.arcs); }},
   };
   return list;
 }

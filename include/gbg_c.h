@@ -65,7 +65,7 @@ typedef struct gbg_caps {
   int has_batch_updates;
 } gbg_caps;
 
-enum { GBG_KIND_CSR = 0, GBG_KIND_BLOCKED = 1 };
+enum { GBG_KIND_CSR = 0, GBG_KIND_BLOCKED = 1, GBG_KIND_COMPRESSED = 2 };
 enum { GBG_MODE_SPARSE = 0, GBG_MODE_DENSE = 1, GBG_MODE_AUTO = 2 };
 
 #define GBG_MAX_LEVELS 64
@@ -112,6 +112,18 @@ gbg_status gbg_blocked_from_csr(gbg_graph* csr, gbg_graph** out);
 gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, double c,
                            uint64_t seed, int kind, gbg_graph** out);
 gbg_status gbg_graph_destroy(gbg_graph* g);
+/* gb::CompressedCsrGraph::build (compressed_csr.cpp:5-17) on the device:
+ * the byte code of bytecode.hpp:11-62 (zig-zag first delta from the vertex
+ * id, then gaps, base-128 varints) with byte_offsets[n+1].  Static
+ * (updates -> GBG_ERR_UNSUPPORTED), capabilities {1,1,1,0,0,0}
+ * (compressed_csr.hpp:27-29).  _from encodes any handle's lists; _create
+ * takes host CSR arrays validated like gbg_csr_create. */
+gbg_status gbg_compressed_from(gbg_graph* src, gbg_graph** out);
+gbg_status gbg_compressed_create(uint64_t n, uint64_t m, const uint64_t* offsets,
+                                 const uint32_t* neighbors, gbg_graph** out);
+/* The raw encoding: byte_offsets[n+1] and bytes[*nbytes] (either may be
+ * NULL to query *nbytes first) — CompressedCsrGraph::segment's data. */
+gbg_status gbg_compressed_bytes(gbg_graph* g, uint64_t* byte_offsets, uint8_t* bytes, uint64_t* nbytes);
 /* GBCSR1 binary graph files (io.cpp:75-114; README.md:134-138): magic
  * "GBCSR1\0\0", n and m as little-endian uint64, n+1 uint64 offsets, m uint32
  * neighbour ids.  load = load_binary_csr (validated like csr.cpp:14-18 and

@@ -306,6 +306,17 @@ class RefCsr:
         self.ref._check(L.gbref_mis(self.h, seed, ptr(out, _u8p)))
         return out
 
+    def compressed(self):
+        """CompressedCsrGraph::build (compressed_csr.cpp:5-17) -> (byte_offsets, bytes)."""
+        L = self.ref.L
+        L.gbref_compressed.argtypes = [C.c_void_p, _u64p, _u8p, _u64p]
+        nb = C.c_uint64()
+        self.ref._check(L.gbref_compressed(self.h, None, None, C.byref(nb)))
+        off = np.empty(self.n + 1, dtype=np.uint64)
+        b = np.empty(max(nb.value, 1), dtype=np.uint8)
+        self.ref._check(L.gbref_compressed(self.h, ptr(off, _u64p), ptr(b, _u8p), C.byref(nb)))
+        return off, b[: nb.value]
+
     def ldd(self, beta=0.2, seed=1):
         """gb::ldd (algorithms.cpp:114-188) -> (labels, parents, rounds)."""
         L = self.ref.L
@@ -474,6 +485,16 @@ class Oracle:
     def _csr_args(self, off, nbr):
         return (ptr(np.ascontiguousarray(off, dtype=np.uint64), _u64p),
                 ptr(np.ascontiguousarray(nbr, dtype=np.uint32), _u32p))
+
+    def bytecode_encode(self, n, off, nbr):
+        """-> (byte_offsets u64[n+1], bytes u8[...])"""
+        self.L.gbo_bytecode_encode.argtypes = [C.c_uint64, _u64p, _u32p, _u64p, _u8p]
+        self.L.gbo_bytecode_encode.restype = C.c_uint64
+        total = self.L.gbo_bytecode_encode(n, *self._csr_args(off, nbr), None, None)
+        bo = np.empty(n + 1, dtype=np.uint64)
+        b = np.empty(max(total, 1), dtype=np.uint8)
+        self.L.gbo_bytecode_encode(n, *self._csr_args(off, nbr), ptr(bo, _u64p), ptr(b, _u8p))
+        return bo, b[:total]
 
     def ldd(self, n, off, nbr, beta=0.2, seed=1):
         self.L.gbo_ldd.argtypes = [C.c_uint64, _u64p, _u32p, C.c_double, C.c_uint64, _u32p, _u32p, _u64p]

@@ -712,3 +712,33 @@ int gbo_ldd(uint64_t n, const uint64_t* off, const uint32_t* nbr, double beta, u
   free(next);
   return 0;
 }
+
+/* bytecode.hpp:11-27 + compressed_csr.cpp:5-17: per vertex, zig-zag of the
+ * first neighbour minus the vertex id, then gaps, as base-128 varints (low 7
+ * bits first, high bit = more); byte_offsets[n+1].  bytes may be NULL to
+ * size the encoding.  Returns the byte count. */
+uint64_t gbo_bytecode_encode(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t* byte_offsets,
+                             uint8_t* bytes) {
+  uint64_t pos = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    if (byte_offsets) byte_offsets[v] = pos;
+    for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+      uint64_t x;
+      if (e == off[v]) {
+        int64_t d = (int64_t)nbr[e] - (int64_t)v;
+        x = d >= 0 ? 2 * (uint64_t)d : 2 * (uint64_t)(-(d + 1)) + 1;
+      } else {
+        x = (uint64_t)(nbr[e] - nbr[e - 1]);
+      }
+      do {
+        uint8_t b = (uint8_t)(x & 0x7f);
+        x >>= 7;
+        if (x) b |= 0x80;
+        if (bytes) bytes[pos] = b;
+        ++pos;
+      } while (x);
+    }
+  }
+  if (byte_offsets) byte_offsets[n] = pos;
+  return pos;
+}

@@ -33,6 +33,8 @@ void gbo_kcore(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t* c
 void gbo_coloring(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* colors);
 int gbo_ldd(uint64_t n, const uint64_t* off, const uint32_t* nbr, double beta, uint64_t seed, uint32_t* labels,
             uint32_t* parents, uint64_t* rounds);
+uint64_t gbo_bytecode_encode(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t* byte_offsets,
+                             uint8_t* bytes);
 void gbo_mis(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint64_t seed, uint8_t* in_set);
 
 void gbo_subset_to_dense(uint64_t n, const uint32_t* ids, uint64_t k, uint64_t* words);

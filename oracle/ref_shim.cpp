@@ -18,6 +18,7 @@
 //   gbref_coloring        gb::coloring                 (algorithms.cpp:376-432)
 //   gbref_mis             gb::mis                      (algorithms.cpp:434-504)
 //   gbref_ldd             gb::ldd                      (algorithms.cpp:114-188)
+//   gbref_compressed      gb::CompressedCsrGraph::build (compressed_csr.cpp:5-17)
 //   gbref_log1p           std::log1p of the reference's C library (rng.hpp:33)
 //   gbref_update_batch    gb::generate_update_batch    (batch.cpp:128-154)
 //   gbref_prepare_global  gb::prepare(GlobalSort)      (batch.cpp:30-42)
@@ -41,6 +42,7 @@
 
 #include "gb/algorithms.hpp"
 #include "gb/batch.hpp"
+#include "gb/compressed_csr.hpp"
 #include "gb/csr.hpp"
 #include "gb/facade.hpp"
 #include "gb/generators.hpp"
@@ -310,6 +312,24 @@ int gbref_ldd(void* csr, double beta, uint64_t seed, uint32_t* labels, uint32_t*
     std::memcpy(labels, r.labels.data(), r.labels.size() * sizeof(uint32_t));
     std::memcpy(parents, r.parents.data(), r.parents.size() * sizeof(uint32_t));
     std::memcpy(rounds, r.rounds.data(), r.rounds.size() * sizeof(uint64_t));
+  });
+}
+
+// byte_offsets[n+1] and the concatenated segments; *nbytes in/out (pass
+// bytes == nullptr to query the size)
+int gbref_compressed(void* csr, uint64_t* byte_offsets, uint8_t* bytes, uint64_t* nbytes) {
+  return guard([&] {
+    const CsrGraph& g = *static_cast<CsrGraph*>(csr);
+    CompressedCsrGraph c = CompressedCsrGraph::build(g);
+    uint64_t pos = 0;
+    for (VertexId v = 0; v < g.num_vertices(); ++v) {
+      auto seg = c.segment(v);
+      if (byte_offsets) byte_offsets[v] = pos;
+      if (bytes) std::memcpy(bytes + pos, seg.data(), seg.size());
+      pos += seg.size();
+    }
+    if (byte_offsets) byte_offsets[g.num_vertices()] = pos;
+    *nbytes = pos;
   });
 }
 

@@ -112,6 +112,11 @@ void build_csr_offsets_from_sorted_src(gbg_graph* g, const uint32_t* src, uint64
   GBG_LAUNCH(g, offsets_from_sorted_k, grid_for(m + 1, 256), 256, 0, src, m, g->n, off);
 }
 
+__global__ void widen_k(const uint32_t* in, uint64_t n, uint64_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) out[v] = in[v];
+}
+
 template <class G>
 __global__ void degrees_k(G gv, uint64_t* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -149,6 +154,9 @@ gbg_graph::~gbg_graph() {
   dfree(bcap);
   dfree(pool);
   dfree(voff);
+  dfree(coff);
+  dfree(cbytes);
+  dfree(cdeg);
   invalidate_derived();
   if (hscalar) cudaFreeHost(hscalar);
   if (stream) {
@@ -245,7 +253,8 @@ static const char kGbcsrMagic[8] = {'G', 'B', 'C', 'S', 'R', '1', '\0', '\0'};
 gbg_status gbg_load_gbcsr1(const char* path, int kind, gbg_graph** out) {
   return guard([&] {
     if (!path || !out) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
-    if (kind != GBG_KIND_CSR && kind != GBG_KIND_BLOCKED) fail(GBG_ERR_CONFIG, "unknown container kind");
+    if (kind != GBG_KIND_CSR && kind != GBG_KIND_BLOCKED && kind != GBG_KIND_COMPRESSED)
+      fail(GBG_ERR_CONFIG, "unknown container kind");
     *out = nullptr;
     std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "rb"), &std::fclose);
     if (!f) fail(GBG_ERR_FORMAT, std::string("cannot open binary graph: ") + path);
@@ -272,7 +281,7 @@ gbg_status gbg_load_gbcsr1(const char* path, int kind, gbg_graph** out) {
     }
     std::unique_ptr<gbg_graph> hold_csr(csr);
     gbg_graph* b = nullptr;
-    st = gbg_blocked_from_csr(csr, &b);
+    st = kind == GBG_KIND_BLOCKED ? gbg_blocked_from_csr(csr, &b) : gbg_compressed_from(csr, &b);
     if (st != GBG_OK) fail(st, gbg_last_error());
     *out = b;
   });
@@ -328,7 +337,7 @@ gbg_status gbg_degree(gbg_graph* g, uint32_t v, uint64_t* deg) {
       *deg = o[1] - o[0];
     } else {
       uint32_t d = 0;
-      read_scalars(g, g->bdeg + v, sizeof(d), &d);
+      read_scalars(g, (g->kind == GBG_KIND_BLOCKED ? g->bdeg : g->cdeg) + v, sizeof(d), &d);
       *deg = d;
     }
   });
@@ -339,9 +348,13 @@ gbg_status gbg_degrees(gbg_graph* g, uint64_t* out) {
     GBG_HANDLE(g);
     if (!out) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
     uint64_t* d = g->ws.get<uint64_t>("degrees", g->n);
-    with_view(g, [&](auto view) {
-      GBG_LAUNCH(g, degrees_k<decltype(view)>, grid_for(g->n, 256), 256, 0, view, d);
-    });
+    if (g->kind == GBG_KIND_COMPRESSED) {
+      GBG_LAUNCH(g, widen_k, grid_for(g->n, 256), 256, 0, g->cdeg, g->n, d);
+    } else {
+      with_view(g, [&](auto view) {
+        GBG_LAUNCH(g, degrees_k<decltype(view)>, grid_for(g->n, 256), 256, 0, view, d);
+      });
+    }
     GBG_CUDA(cudaMemcpyAsync(out, d, g->n * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
     GBG_CUDA(cudaStreamSynchronize(g->stream));
   });
@@ -354,7 +367,14 @@ gbg_status gbg_neighbors(gbg_graph* g, uint32_t v, uint32_t* out, uint64_t cap, 
     if (v >= g->n) fail(GBG_ERR_OUT_OF_RANGE, "neighbors: vertex out of range");
     uint64_t begin = 0, d = 0;
     const uint32_t* base;
-    if (g->kind == GBG_KIND_CSR) {
+    if (g->kind == GBG_KIND_COMPRESSED) {
+      uint32_t dd = 0;
+      read_scalars(g, g->cdeg + v, sizeof(dd), &dd);
+      uint32_t* tmp = g->ws.get<uint32_t>("nbrs", dd);
+      if (dd) compressed_neighbors(g, v, tmp);
+      d = dd;
+      base = tmp;
+    } else if (g->kind == GBG_KIND_CSR) {
       uint64_t o[2];
       read_scalars(g, g->off + v, sizeof(o), o);
       begin = o[0];
@@ -382,10 +402,11 @@ gbg_status gbg_export_csr(gbg_graph* g, uint64_t* offsets, uint32_t* neighbors) 
   return guard([&] {
     GBG_HANDLE(g);
     if (!offsets || (g->m && !neighbors)) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
-    if (g->kind == GBG_KIND_CSR) {
-      GBG_CUDA(cudaMemcpyAsync(offsets, g->off, (g->n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
+    if (g->kind == GBG_KIND_CSR || g->kind == GBG_KIND_COMPRESSED) {
+      const CsrView v = g->kind == GBG_KIND_CSR ? g->csr_view() : compressed_decoded(g);
+      GBG_CUDA(cudaMemcpyAsync(offsets, v.off, (g->n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
       if (g->m)
-        GBG_CUDA(cudaMemcpyAsync(neighbors, g->nbr, g->m * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+        GBG_CUDA(cudaMemcpyAsync(neighbors, v.nbr, g->m * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
     } else {
       const uint64_t* voff = virtual_offsets(g);
       uint32_t* tmp = g->ws.get<uint32_t>("export", g->m);
@@ -406,7 +427,12 @@ gbg_status gbg_capabilities(const gbg_graph* g, gbg_caps* caps) {
     if (!g || !caps) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
     // CSR pattern (csr.hpp:31-33); the blocked container adds batch updates
     // (set_graph.hpp:95-98).
-    *caps = gbg_caps{1, 1, 1, 1, 1, g->kind == GBG_KIND_BLOCKED ? 1 : 0};
+    // The compressed container decodes sequentially: no parallel maps
+    // (compressed_csr.hpp:27-29).
+    if (g->kind == GBG_KIND_COMPRESSED)
+      *caps = gbg_caps{1, 1, 1, 0, 0, 0};
+    else
+      *caps = gbg_caps{1, 1, 1, 1, 1, g->kind == GBG_KIND_BLOCKED ? 1 : 0};
   });
 }
 
@@ -415,6 +441,8 @@ gbg_status gbg_memory_bytes(const gbg_graph* g, uint64_t* bytes) {
     if (!g || !bytes) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
     if (g->kind == GBG_KIND_CSR)
       *bytes = (g->n + 1) * sizeof(uint64_t) + g->m * sizeof(uint32_t);
+    else if (g->kind == GBG_KIND_COMPRESSED)  // compressed_csr.hpp:31-33 plus the degree array
+      *bytes = (g->n + 1) * sizeof(uint64_t) + g->cbytes_len + g->n * sizeof(uint32_t);
     else
       *bytes = g->n * (sizeof(uint64_t) + 2 * sizeof(uint32_t)) + g->pool_cap * sizeof(uint32_t);
   });

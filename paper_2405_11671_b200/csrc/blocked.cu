@@ -125,6 +125,7 @@ struct DegIn {
 
 const uint64_t* virtual_offsets(gbg_graph* g) {
   if (g->kind == GBG_KIND_CSR) return g->off;
+  if (g->kind == GBG_KIND_COMPRESSED) return compressed_decoded(g).off;
   if (!g->voff) g->voff = dalloc<uint64_t>(g->n + 1);
   if (!g->voff_valid) {
     device_scan<uint64_t>(g, DegIn{g->bdeg}, ArrayOut<uint64_t>{g->voff}, g->n, g->voff + g->n, "blk.voff");

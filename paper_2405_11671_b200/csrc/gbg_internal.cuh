@@ -178,6 +178,13 @@ struct gbg_graph {
   uint64_t pool_top = 0;       // ids handed out (bump allocator)
   uint64_t pool_live = 0;      // ids in live allocations
 
+  // compressed storage (compressed.cu)
+  uint64_t* coff = nullptr;    // byte offsets [n+1]
+  uint8_t* cbytes = nullptr;   // byte code (+8 padding bytes)
+  uint64_t cbytes_len = 0;
+  uint32_t* cdeg = nullptr;    // degrees
+  bool cz_ready = false;       // transient decoded CSR present in ws ("cz.off"/"cz.nbr")
+
   // derived, rebuilt lazily after updates
   uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
   bool voff_valid = false;
@@ -213,13 +220,21 @@ inline unsigned grid_for(uint64_t items, unsigned per_block, unsigned cap = 148u
 // Read small device scalars back (synchronises the handle's stream).
 void read_scalars(gbg_graph* g, const void* dev, size_t bytes, void* host);
 
+// Compressed handles: the decoded CSR for the current API call (built on
+// first use, released by TransientScope), one vertex's list, release.
+CsrView compressed_decoded(gbg_graph* g);
+void compressed_neighbors(gbg_graph* g, uint32_t v, uint32_t* out_dev);
+void release_transient(gbg_graph* g);
+
 // Dispatch a functor templated on the view type.
 template <class F>
 void with_view(gbg_graph* g, F&& f) {
   if (g->kind == GBG_KIND_CSR)
     f(g->csr_view());
-  else
+  else if (g->kind == GBG_KIND_BLOCKED)
     f(g->blocked_view());
+  else
+    f(compressed_decoded(g));
 }
 
 // Ensure the blocked container's virtual offsets (scan of degrees) are
@@ -304,12 +319,20 @@ struct DeviceScope {
   }
 };
 
+// Drops per-call transient state (a compressed handle's decoded CSR) when
+// the API call returns; frees are stream-ordered after the call's work.
+struct TransientScope {
+  gbg_graph* g;
+  ~TransientScope() { release_transient(g); }
+};
+
 // Locked, device-scoped access to a handle.
 #define GBG_HANDLE(g)                                                        \
   if (!(g)) ::gbg::fail(GBG_ERR_INVALID_ARGUMENT, "null graph handle");     \
   std::lock_guard<std::mutex> gbg_lock_((g)->mu);                            \
   ::gbg::DeviceScope gbg_dev_((g)->device);                                  \
-  ::gbg::AllocStream gbg_as_((g)->stream)
+  ::gbg::AllocStream gbg_as_((g)->stream);                                   \
+  ::gbg::TransientScope gbg_tr_{(g)}
 
 gbg_graph* new_handle(int kind, uint64_t n);
 void build_csr_offsets_from_sorted_src(gbg_graph* g, const uint32_t* src, uint64_t m, uint64_t* off);

@@ -107,7 +107,8 @@ gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, d
                            gbg_graph** out) {
   return guard([&] {
     if (!out) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
-    if (kind != GBG_KIND_CSR && kind != GBG_KIND_BLOCKED) fail(GBG_ERR_CONFIG, "rmat: unknown container kind");
+    if (kind != GBG_KIND_CSR && kind != GBG_KIND_BLOCKED && kind != GBG_KIND_COMPRESSED)
+      fail(GBG_ERR_CONFIG, "rmat: unknown container kind");
     *out = nullptr;
     RmatParams p = make_params(log2_n, a, b, c, seed);
     const uint64_t n = uint64_t{1} << log2_n;
@@ -148,6 +149,11 @@ gbg_status gbg_rmat_create(uint32_t log2_n, uint64_t arcs, double a, double b, d
       blocked_from_device_csr(b.get(), n, g->off, g->nbr);
       GBG_CUDA(cudaStreamSynchronize(b->stream));
       *out = b.release();
+    } else if (kind == GBG_KIND_COMPRESSED) {
+      gbg_graph* z = nullptr;
+      const gbg_status st = gbg_compressed_from(g.get(), &z);
+      if (st != GBG_OK) fail(st, gbg_last_error());
+      *out = z;
     } else {
       *out = g.release();
     }

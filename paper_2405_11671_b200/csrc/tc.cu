@@ -115,10 +115,11 @@ uint64_t tc_run(gbg_graph* g) {
   const uint64_t n = g->n, m = g->m;
   if (m == 0) return 0;
   // a packed CSR view (the blocked container is gathered into one first)
-  const uint64_t* off = g->off;
-  const uint32_t* nbr = g->nbr;
+  const CsrView csr = g->kind == GBG_KIND_COMPRESSED ? compressed_decoded(g) : g->csr_view();
+  const uint64_t* off = csr.off;
+  const uint32_t* nbr = csr.nbr;
   uint32_t* src = g->ws.get<uint32_t>("tc.src", m);
-  if (g->kind != GBG_KIND_CSR) {
+  if (g->kind == GBG_KIND_BLOCKED) {
     const uint64_t* voff = virtual_offsets(g);
     uint32_t* packed = g->ws.get<uint32_t>("tc.packed", m);
     BlockedView bv = g->blocked_view();
@@ -129,7 +130,7 @@ uint64_t tc_run(gbg_graph* g) {
     off = voff;
     nbr = packed;
   } else {
-    for_each_edge(g, g->csr_view(), off, m, SrcOp<CsrView>{src});
+    for_each_edge(g, csr, off, m, SrcOp<CsrView>{src});
   }
   uint32_t* osrc = g->ws.get<uint32_t>("tc.osrc", m);
   uint32_t* onbr = g->ws.get<uint32_t>("tc.onbr", m);

@@ -34,7 +34,7 @@ _L = C.CDLL(LIB_PATH)
 # ---------------------------------------------------------------- errors
 GBG_OK, GBG_ERR_CUDA, GBG_ERR_OOM, GBG_ERR_OUT_OF_RANGE, GBG_ERR_INVALID_ARGUMENT = 0, 1, 2, 3, 4
 GBG_ERR_UNSUPPORTED, GBG_ERR_CONFIG, GBG_ERR_FORMAT, GBG_ERR_LOGIC = 5, 6, 7, 8
-KIND_CSR, KIND_BLOCKED = 0, 1
+KIND_CSR, KIND_BLOCKED, KIND_COMPRESSED = 0, 1, 2
 MODE_SPARSE, MODE_DENSE, MODE_AUTO = 0, 1, 2
 MAX_LEVELS = 64
 
@@ -156,6 +156,9 @@ _SIGS = {
     "gbg_kcore": [_vp, _u64p],
     "gbg_coloring": [_vp, _u32p],
     "gbg_mis": [_vp, C.c_uint64, _u8p],
+    "gbg_compressed_from": [_vp, _gpp],
+    "gbg_compressed_create": [C.c_uint64, C.c_uint64, _u64p, _u32p, _gpp],
+    "gbg_compressed_bytes": [_vp, _u64p, _u8p, _u64p],
     "gbg_ldd": [_vp, C.c_double, C.c_uint64, _u32p, _u32p, _u64p],
     "gbg_selftest_log1p": [_f64p, C.c_uint64, _f64p],
     "gbg_load_gbcsr1": [C.c_char_p, C.c_int, _gpp],
@@ -196,10 +199,19 @@ class _Graph:
         self._h = handle
 
     def __del__(self):
+        self.close()
+
+    def close(self):
         h = getattr(self, "_h", None)
         if h:
             _L.gbg_graph_destroy(h)
             self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     @property
     def handle(self):
@@ -343,19 +355,57 @@ class BlockedGraph(_Graph):
         return cls(h.value)
 
 
+class CompressedGraph(_Graph):
+    """gb::CompressedCsrGraph (compressed_csr.hpp:12-46) on the device: the
+    byte code of bytecode.hpp, static, no parallel maps."""
+
+    @classmethod
+    def build(cls, n: int, arcs) -> "CompressedGraph":
+        with CsrGraph.build(n, arcs) as csr:
+            return cls.from_graph(csr)
+
+    @classmethod
+    def from_csr(cls, offsets, neighbors) -> "CompressedGraph":
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        h = C.c_void_p()
+        _check(_L.gbg_compressed_create(off.size - 1, nbr.size, _p(off, _u64p), _p(nbr, _u32p), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_graph(cls, g: _Graph) -> "CompressedGraph":
+        """CompressedCsrGraph::build (compressed_csr.cpp:5-17) from any handle."""
+        h = C.c_void_p()
+        _check(_L.gbg_compressed_from(g.handle, C.byref(h)))
+        return cls(h.value)
+
+    def encoding(self):
+        """(byte_offsets u64[n+1], bytes u8[...]): the raw byte code."""
+        nb = C.c_uint64()
+        _check(_L.gbg_compressed_bytes(self.handle, None, None, C.byref(nb)))
+        off = np.empty(self.num_vertices() + 1, dtype=np.uint64)
+        b = np.empty(max(nb.value, 1), dtype=np.uint8)
+        _check(_L.gbg_compressed_bytes(self.handle, _p(off, _u64p), _p(b, _u8p), C.byref(nb)))
+        return off, b[: nb.value]
+
+
+def _cls_of(kind: int):
+    return {KIND_CSR: CsrGraph, KIND_BLOCKED: BlockedGraph, KIND_COMPRESSED: CompressedGraph}[kind]
+
+
 def generate_rmat(log2_n: int, arcs: int, seed: int, a=0.5, b=0.1, c=0.1, kind: int = KIND_CSR):
     """gb::generate_rmat (generators.cpp:67-72) on the device, bit-exact.
     Defaults are RmatParams' (batch.hpp:44-50)."""
     h = C.c_void_p()
     _check(_L.gbg_rmat_create(log2_n, arcs, a, b, c, seed, kind, C.byref(h)))
-    return (CsrGraph if kind == KIND_CSR else BlockedGraph)(h.value)
+    return _cls_of(kind)(h.value)
 
 
 def load_binary(path: str, kind: int = KIND_CSR):
     """gb::load_binary_csr (io.cpp:87-110): a GBCSR1 file into a device container."""
     h = C.c_void_p()
     _check(_L.gbg_load_gbcsr1(os.fsencode(path), kind, C.byref(h)))
-    return (CsrGraph if kind == KIND_CSR else BlockedGraph)(h.value)
+    return _cls_of(kind)(h.value)
 
 
 def save_binary(g: _Graph, path: str):

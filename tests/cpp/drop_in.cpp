@@ -149,6 +149,9 @@ int main() {
     try { g->insert_sorted_batch({}); } catch (const unsupported_operation&) { ++thrown; }
     try { g->delete_sorted_batch({}); } catch (const unsupported_operation&) { ++thrown; }
     if (thrown != 4) return d = "updates accepted", false;
+    GraphContainerPtr z = extra[2].build(t4);  // compressed: static too
+    try { z->insert_edge({0, 3}); return d = "compressed accepted an update", false; } catch (const unsupported_operation&) {}
+    if (z->capabilities().has_parallel_map) return d = "compressed offers parallel maps", false;
     std::vector<Edge> unsorted = {{1, 0}, {0, 1}}, dup = {{0, 1}, {0, 1}}, oor = {{0, 5}};
     int fmt = 0;
     for (auto* a : {&unsorted, &dup, &oor}) {

@@ -474,3 +474,21 @@ def test_ldd_matches_reference(ref, orc):
     off, nbr = csr(n, pairs)
     for a, b in zip(orc.ldd(n, off, nbr, 0.2, 1), ref.csr(n, off, nbr).ldd(0.2, 1)):
         assert np.array_equal(a, b)
+
+
+def test_bytecode_known_answers_and_reference(ref, orc):
+    # test_containers.cpp:54-65: pinned wire examples
+    off, nbr = csr(11, [(6, 5), (6, 7), (6, 10)])
+    bo, b = orc.bytecode_encode(11, off, nbr)
+    assert b[bo[6]:bo[7]].tolist() == [0x01, 0x02, 0x03] and bo[7] - bo[6] == 3 and bo[11] == 3
+    off, nbr = csr(201, [(0, 200)])
+    bo, b = orc.bytecode_encode(201, off, nbr)
+    assert b.tolist() == [0x90, 0x03]
+    off, nbr = csr(3, np.zeros((0, 2), np.uint32))
+    bo, b = orc.bytecode_encode(3, off, nbr)
+    assert b.size == 0 and bo.tolist() == [0, 0, 0, 0]
+    for n, pairs in [ref.er(300, 0.05, 41), ref.rmat(12, 16 << 12, 1), (120, _directed(120, 0.1, 2))]:
+        off, nbr = csr(n, pairs)
+        want = ref.csr(n, off, nbr).compressed()
+        got = orc.bytecode_encode(n, off, nbr)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
