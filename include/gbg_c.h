@@ -96,6 +96,14 @@ gbg_status gbg_synchronize(gbg_graph* g);
  * segments with GBG_ERR_FORMAT, like csr.cpp:14-18. */
 gbg_status gbg_csr_create(uint64_t n, uint64_t m, const uint64_t* offsets,
                           const uint32_t* neighbors, gbg_graph** out);
+/* gbg_csr_create with build flags.  GBG_CREATE_PAGERANK_LAYOUT also builds
+ * the degree-ordered PageRank layout while the neighbour ids upload (it is
+ * otherwise built by the first gbg_pagerank call).  The upload is chunked
+ * and overlapped with validation either way; pinned host buffers make it
+ * asynchronous. */
+enum { GBG_CREATE_PAGERANK_LAYOUT = 1 };
+gbg_status gbg_csr_create_ex(uint64_t n, uint64_t m, const uint64_t* offsets,
+                             const uint32_t* neighbors, uint32_t flags, gbg_graph** out);
 /* gb::CsrGraph::build(n, arcs) from sorted, deduplicated (src,dst) pairs. */
 gbg_status gbg_csr_from_arcs(uint64_t n, const uint32_t* arcs, uint64_t m, gbg_graph** out);
 /* The dynamic blocked sorted-adjacency container: the role of

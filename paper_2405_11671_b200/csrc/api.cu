@@ -189,10 +189,17 @@ gbg_status gbg_synchronize(gbg_graph* g) {
   });
 }
 
-gbg_status gbg_csr_create(uint64_t n, uint64_t m, const uint64_t* offsets, const uint32_t* neighbors,
-                          gbg_graph** out) {
+// The upload is pipelined: offsets first, then the neighbour ids in chunks
+// on a copy stream, each chunk validated (and, with
+// GBG_CREATE_PAGERANK_LAYOUT, relabelled into the PageRank layout) on the
+// handle's stream as soon as it lands, so host->device transfer hides the
+// checks and the layout build.  Pinned host buffers make the copies
+// asynchronous; pageable ones still work (the driver stages them).
+gbg_status gbg_csr_create_ex(uint64_t n, uint64_t m, const uint64_t* offsets, const uint32_t* neighbors,
+                             uint32_t flags, gbg_graph** out) {
   return guard([&] {
     if (!out || !offsets || (m && !neighbors)) fail(GBG_ERR_INVALID_ARGUMENT, "gbg_csr_create: null argument");
+    if (flags & ~uint32_t{GBG_CREATE_PAGERANK_LAYOUT}) fail(GBG_ERR_INVALID_ARGUMENT, "gbg_csr_create: unknown flags");
     *out = nullptr;
     gbg_graph* g = new_handle(GBG_KIND_CSR, n);
     std::unique_ptr<gbg_graph> hold(g);
@@ -200,20 +207,74 @@ gbg_status gbg_csr_create(uint64_t n, uint64_t m, const uint64_t* offsets, const
     g->m = m;
     g->off = dalloc<uint64_t>(n + 1);
     g->nbr = dalloc<uint32_t>(m);
-    GBG_CUDA(cudaMemcpyAsync(g->off, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, g->stream));
-    if (m)
-      GBG_CUDA(cudaMemcpyAsync(g->nbr, neighbors, m * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream));
+    GBG_CUDA(cudaStreamSynchronize(g->stream));  // allocations visible to the copy stream
+    constexpr uint64_t kChunkIds = uint64_t{1} << 26;  // 256 MB of ids per chunk
+    const uint64_t nchunks = (m + kChunkIds - 1) / kChunkIds;
+    struct Copier {  // copy stream + per-chunk events; drained before the handle can be freed
+      cudaStream_t cs = nullptr;
+      std::vector<cudaEvent_t> ev;
+      ~Copier() {
+        if (cs) {
+          cudaStreamSynchronize(cs);
+          cudaStreamDestroy(cs);
+        }
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+      }
+    } cp;
+    GBG_CUDA(cudaStreamCreateWithFlags(&cp.cs, cudaStreamNonBlocking));
+    cp.ev.resize(nchunks + 1);
+    for (auto& e : cp.ev) GBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    GBG_CUDA(cudaMemcpyAsync(g->off, offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, cp.cs));
+    GBG_CUDA(cudaEventRecord(cp.ev[0], cp.cs));
+    for (uint64_t c = 0; c < nchunks; ++c) {
+      const uint64_t e0 = c * kChunkIds, e1 = std::min(m, e0 + kChunkIds);
+      GBG_CUDA(cudaMemcpyAsync(g->nbr + e0, neighbors + e0, (e1 - e0) * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               cp.cs));
+      GBG_CUDA(cudaEventRecord(cp.ev[c + 1], cp.cs));
+    }
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    GBG_CUDA(cudaEventCreate(&t0));
+    GBG_CUDA(cudaEventCreate(&t1));
+    GBG_CUDA(cudaStreamWaitEvent(g->stream, cp.ev[0], 0));
+    GBG_CUDA(cudaEventRecord(t0, g->stream));
     int* bad = g->ws.get<int>("bad", 1);
     GBG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
     GBG_LAUNCH(g, csr_validate_offsets_k, grid_for(n + 1, 256), 256, 0, n, m, g->off, bad);
     int hb = 0;
     read_scalars(g, bad, sizeof(int), &hb);
     if (hb) fail(GBG_ERR_FORMAT, "csr_build: offsets must rise monotonically from 0 to m");
-    for_each_edge(g, g->csr_view(), g->off, m, SegmentOrderOp{g->off, g->nbr, n, bad});
+    PrLayout* L = nullptr;
+    struct LayoutHold {
+      PrLayout*& L;
+      ~LayoutHold() {
+        if (L) pr_layout_free(L);
+      }
+    } lh{L};
+    if ((flags & GBG_CREATE_PAGERANK_LAYOUT) && n) L = pr_layout_rows_csr(g);  // offsets only
+    for (uint64_t c = 0; c < nchunks; ++c) {
+      const uint64_t e0 = c * kChunkIds, e1 = std::min(m, e0 + kChunkIds);
+      GBG_CUDA(cudaStreamWaitEvent(g->stream, cp.ev[c + 1], 0));
+      for_each_edge_range(g, g->csr_view(), g->off, e0, e1, SegmentOrderOp{g->off, g->nbr, n, bad});
+      if (L) pr_layout_relabel_csr(g, L, e0, e1);
+    }
+    GBG_CUDA(cudaEventRecord(t1, g->stream));
     read_scalars(g, bad, sizeof(int), &hb);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
     if (hb) fail(GBG_ERR_FORMAT, "csr_build: arcs must be sorted, deduplicated and in range");
+    if (L) {
+      pr_layout_attach(g, L, ms);
+      L = nullptr;
+    }
     *out = hold.release();
   });
+}
+
+gbg_status gbg_csr_create(uint64_t n, uint64_t m, const uint64_t* offsets, const uint32_t* neighbors,
+                          gbg_graph** out) {
+  return gbg_csr_create_ex(n, m, offsets, neighbors, 0, out);
 }
 
 gbg_status gbg_csr_from_arcs(uint64_t n, const uint32_t* arcs, uint64_t m, gbg_graph** out) {

@@ -27,9 +27,9 @@ __device__ __forceinline__ uint32_t row_of(const uint64_t* voff, uint64_t n, uin
 // op(u, v, e): arc u -> v, e = its index in voff order
 template <class G, class Op>
 __global__ void __launch_bounds__(kEdgeThreads) for_each_edge_k(G g, const uint64_t* __restrict__ voff, uint64_t m,
-                                                                 Op op) {
+                                                                 Op op, uint64_t base) {
   __shared__ uint32_t s_row[kEdgeTile];
-  const uint64_t e0 = static_cast<uint64_t>(blockIdx.x) * kEdgeTile;
+  const uint64_t e0 = base + static_cast<uint64_t>(blockIdx.x) * kEdgeTile;
   if (e0 >= m) return;
   const uint32_t len = static_cast<uint32_t>(m - e0 < kEdgeTile ? m - e0 : kEdgeTile);
   {
@@ -119,7 +119,16 @@ template <class G, class Op>
 void for_each_edge(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Op op) {
   if (m == 0) return;
   const uint64_t tiles = (m + kEdgeTile - 1) / kEdgeTile;
-  GBG_LAUNCH(g, (for_each_edge_k<G, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, m, op);
+  GBG_LAUNCH(g, (for_each_edge_k<G, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, m, op,
+             uint64_t{0});
+}
+
+// the edges [e0, e1) only (same op(u, v, e) contract, e absolute)
+template <class G, class Op>
+void for_each_edge_range(gbg_graph* g, G view, const uint64_t* voff, uint64_t e0, uint64_t e1, Op op) {
+  if (e1 <= e0) return;
+  const uint64_t tiles = (e1 - e0 + kEdgeTile - 1) / kEdgeTile;
+  GBG_LAUNCH(g, (for_each_edge_k<G, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, view, voff, e1, op, e0);
 }
 
 // counts[u] += |{v in N(u) : pred(u, v)}| over the same balanced tiles.  A

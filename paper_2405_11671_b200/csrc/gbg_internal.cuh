@@ -244,6 +244,12 @@ const uint64_t* virtual_offsets(gbg_graph* g);
 // Every arc has its reverse (checked once per graph version, cc.cu).
 bool graph_is_symmetric(gbg_graph* g);
 
+// PageRank layout in phases for pipelined CSR builds (pagerank.cu).
+PrLayout* pr_layout_rows_csr(gbg_graph* g);
+void pr_layout_relabel_csr(gbg_graph* g, PrLayout* L, uint64_t e0, uint64_t e1);
+void pr_layout_attach(gbg_graph* g, PrLayout* L, float build_ms);
+void pr_layout_free(PrLayout* L);
+
 // Optional phase timing (environment GBG_TRACE=1): CUDA events on the
 // handle's stream at named points, device-time deltas printed to stderr
 // when the tracer goes out of scope.

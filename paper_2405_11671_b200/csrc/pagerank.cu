@@ -155,12 +155,13 @@ struct HeavyChunksOut {
   }
 };
 
+// Phase 1 (offsets only): the degree order, the relabelled offsets, the
+// degree classes and the heavy-row chunk map; L->nbr is allocated but not
+// filled.  Phase 2 (layout_relabel) fills it for any range of edges, so a
+// pipelined container build can relabel each chunk of neighbour ids as it
+// lands (gbg_csr_create_ex, api.cu).
 template <class G>
-PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
-  cudaEvent_t e0, e1;
-  GBG_CUDA(cudaEventCreate(&e0));
-  GBG_CUDA(cudaEventCreate(&e1));
-  GBG_CUDA(cudaEventRecord(e0, g->stream));
+PrLayout* layout_rows(gbg_graph* g, G view) {
   const uint64_t n = g->n, m = g->m;
   auto L = std::make_unique<PrLayout>();
   L->n = n;
@@ -179,7 +180,6 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   L->nbr = dalloc<uint32_t>(m);
   GBG_LAUNCH(g, order_from_keys_k, grid_for(n, 256), 256, 0, sorted, n, L->ord, L->pos);
   device_scan<uint64_t>(g, SortedDegIn{sorted}, ArrayOut<uint64_t>{L->off}, n, L->off + n, "prl.scan");
-  for_each_edge(g, view, voff, m, RelabelOp{voff, L->pos, L->off, L->nbr});
   uint32_t* bnd = g->ws.get<uint32_t>("prl.bnd", kClasses);
   GBG_LAUNCH(g, class_bounds_k, 1, 32, 0, L->off, n, bnd);
   uint32_t hb[kClasses];
@@ -211,6 +211,32 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   g->ws.release("prl.keys");
   g->ws.release("prl.sorted");
   g->ws.release("prl.cub");
+  return L.release();
+}
+
+// relabel op for not-yet-validated input: out-of-range ids are skipped (the
+// caller's validation rejects the graph)
+struct RelabelCheckedOp {
+  RelabelOp op;
+  uint64_t n;
+  __device__ __forceinline__ void operator()(uint32_t u, uint32_t v, uint64_t e) const {
+    if (v < n) op(u, v, e);
+  }
+};
+
+template <class G>
+void layout_relabel(gbg_graph* g, G view, const uint64_t* voff, PrLayout* L, uint64_t e0, uint64_t e1) {
+  for_each_edge_range(g, view, voff, e0, e1, RelabelCheckedOp{RelabelOp{voff, L->pos, L->off, L->nbr}, g->n});
+}
+
+template <class G>
+PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
+  cudaEvent_t e0, e1;
+  GBG_CUDA(cudaEventCreate(&e0));
+  GBG_CUDA(cudaEventCreate(&e1));
+  GBG_CUDA(cudaEventRecord(e0, g->stream));
+  PrLayout* L = layout_rows(g, view);
+  layout_relabel(g, view, voff, L, 0, g->m);
   GBG_CUDA(cudaEventRecord(e1, g->stream));
   GBG_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
@@ -218,7 +244,7 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   L->build_ms = ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  return L.release();
+  return L;
 }
 
 // ---------------------------------------------------------------- iteration
@@ -429,6 +455,8 @@ PrLayout* pr_layout(gbg_graph* g) {
   if (!g->pr) {
     const uint64_t* voff = virtual_offsets(g);
     with_view(g, [&](auto view) { g->pr = build_layout(g, view, voff); });
+  }
+  if (!g->pr->grid) {
     int per_sm = 1;
     GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pr_iter_k, kPrThreads, 0));
     g->pr->grid = static_cast<uint32_t>(std::max(per_sm, 1) * g->sm_count);
@@ -436,6 +464,17 @@ PrLayout* pr_layout(gbg_graph* g) {
   }
   return g->pr;
 }
+
+// pipelined CSR builds (api.cu)
+PrLayout* pr_layout_rows_csr(gbg_graph* g) { return layout_rows(g, g->csr_view()); }
+void pr_layout_relabel_csr(gbg_graph* g, PrLayout* L, uint64_t e0, uint64_t e1) {
+  layout_relabel(g, g->csr_view(), g->off, L, e0, e1);
+}
+void pr_layout_attach(gbg_graph* g, PrLayout* L, float build_ms) {
+  L->build_ms = build_ms;
+  g->pr = L;
+}
+void pr_layout_free(PrLayout* L) { delete L; }
 
 uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double tol, double* p_dev) {
   const uint64_t n = g->n;

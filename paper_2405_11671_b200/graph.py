@@ -35,6 +35,7 @@ _L = C.CDLL(LIB_PATH)
 GBG_OK, GBG_ERR_CUDA, GBG_ERR_OOM, GBG_ERR_OUT_OF_RANGE, GBG_ERR_INVALID_ARGUMENT = 0, 1, 2, 3, 4
 GBG_ERR_UNSUPPORTED, GBG_ERR_CONFIG, GBG_ERR_FORMAT, GBG_ERR_LOGIC = 5, 6, 7, 8
 KIND_CSR, KIND_BLOCKED, KIND_COMPRESSED = 0, 1, 2
+GBG_CREATE_PAGERANK_LAYOUT = 1
 MODE_SPARSE, MODE_DENSE, MODE_AUTO = 0, 1, 2
 MAX_LEVELS = 64
 
@@ -119,6 +120,7 @@ _SIGS = {
     "gbg_synchronize": [_vp],
     "gbg_csr_create": [C.c_uint64, C.c_uint64, _u64p, _u32p, _gpp],
     "gbg_csr_from_arcs": [C.c_uint64, _u32p, C.c_uint64, _gpp],
+    "gbg_csr_create_ex": [C.c_uint64, C.c_uint64, _u64p, _u32p, C.c_uint32, _gpp],
     "gbg_blocked_create": [C.c_uint64, _u32p, C.c_uint64, _gpp],
     "gbg_blocked_from_csr": [_vp, _gpp],
     "gbg_rmat_create": [C.c_uint32, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int, _gpp],
@@ -329,11 +331,15 @@ class CsrGraph(_Graph):
         return cls(h.value)
 
     @classmethod
-    def from_csr(cls, offsets, neighbors) -> "CsrGraph":
+    def from_csr(cls, offsets, neighbors, prepare_pagerank: bool = False) -> "CsrGraph":
+        """CsrGraph::build from CSR arrays (validated like csr.cpp:14-18).
+        The upload is chunked and overlapped with validation; with
+        prepare_pagerank the PageRank layout is built during the upload."""
         off = np.ascontiguousarray(offsets, dtype=np.uint64)
         nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
         h = C.c_void_p()
-        _check(_L.gbg_csr_create(off.size - 1, nbr.size, _p(off, _u64p), _p(nbr, _u32p), C.byref(h)))
+        flags = GBG_CREATE_PAGERANK_LAYOUT if prepare_pagerank else 0
+        _check(_L.gbg_csr_create_ex(off.size - 1, nbr.size, _p(off, _u64p), _p(nbr, _u32p), flags, C.byref(h)))
         return cls(h.value)
 
 

@@ -126,3 +126,29 @@ def test_pool_growth_and_relayout(gbg, orc):
     assert np.array_equal(go, off) and np.array_equal(gn, nbr)
     assert np.array_equal(gbg.bfs(g, 0).depth, orc.bfs(n, off, nbr, 0)[0])
     assert g.memory_bytes() > 0
+
+
+def test_pipelined_create_with_pagerank_layout(gbg, ref, orc):
+    """gbg_csr_create_ex: chunked upload + validation, optional PageRank
+    layout built during the upload — same ranks, same rejections."""
+    n, pairs = ref.rmat(14, 16 << 14, 1)
+    off, nbr = csr(n, pairs)
+    a = gbg.CsrGraph.from_csr(off, nbr, prepare_pagerank=True)
+    b = gbg.CsrGraph.from_csr(off, nbr)
+    pa = gbg.pagerank(a, 0.85, 20, 1e-300)
+    pb = gbg.pagerank(b, 0.85, 20, 1e-300)
+    assert np.array_equal(pa, pb)
+    want = orc.pagerank(n, off, nbr, 0.85, 20, 1e-300)
+    assert np.abs(pa - want).sum() / np.abs(want).sum() <= 1e-9
+    bad = nbr.copy()
+    bad[5] = n + 3  # out of range: rejected, no crash in the layout relabel
+    with pytest.raises(gbg.FormatError):
+        gbg.CsrGraph.from_csr(off, bad, prepare_pagerank=True)
+    bad = nbr.copy()
+    bad[[10, 11]] = bad[[11, 10]]  # unsorted segment
+    with pytest.raises(gbg.FormatError):
+        gbg.CsrGraph.from_csr(off, bad, prepare_pagerank=True)
+    boff = off.copy()
+    boff[3] = boff[4] + 1
+    with pytest.raises(gbg.FormatError):
+        gbg.CsrGraph.from_csr(boff, nbr, prepare_pagerank=True)
