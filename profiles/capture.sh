@@ -15,7 +15,8 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launches=$?"
 # kernel regex : launches to skip (past warm-up / first graph) : count
 for spec in "pr_iter_k:25:1" "pull_k:2:2" "push_k:3:2" "expand_k:6:3" "apply_flags_k:2:1" \
-            "tc_count_k:0:1" "cc_sample_k:0:1" "DeviceRadixSortOnesweepKernel:12:1" "rmat_keys_k:0:1"; do
+            "tc_count_k:0:1" "cc_sample_k:0:1" "DeviceRadixSortOnesweepKernel:12:1" "rmat_keys_k:0:1" \
+            ${EXTRA_SPECS:-}; do
   k=${spec%%:*}; rest=${spec#*:}; s=${rest%%:*}; c=${rest#*:}
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$k" -s "$s" -c "$c" \
     -o "$OUT/${TAG}_full_$k" $P > "$OUT/${TAG}_ncu_$k.log" 2>&1
