@@ -134,3 +134,29 @@ def test_scale24_match_golden(gbg):
     assert digest(gbg.kcore(g)) == gd["kcore"]["digest"]
     assert digest(gbg.coloring(g)) == gd["coloring"]["digest"]
     assert digest(gbg.mis(g, gd["mis"]["seed"])) == gd["mis"]["digest"]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_empty_single_and_self_loops(gbg, ref, orc, kind):
+    """n = 0 and n = 1 handles; self-loops (CsrGraph::build accepts them,
+    csr.cpp:9-25) take the reference's paths: a self-loop never beats its
+    own vertex and is released like any other arc."""
+    z = build(gbg, kind, 0, [])
+    assert gbg.kcore(z).size == 0 and gbg.coloring(z).size == 0 and gbg.mis(z, 1).size == 0
+    assert gbg.ldd(z, 0.2, 1)[0].size == 0
+    one = build(gbg, kind, 1, [])
+    assert gbg.kcore(one).tolist() == [0] and gbg.coloring(one).tolist() == [0] and gbg.mis(one, 1).tolist() == [1]
+    rng = np.random.default_rng(11)
+    for trial in range(4):
+        n, pairs = ref.er(80, 0.08, 50 + trial)
+        loops = np.repeat(rng.choice(n, 10, replace=False).astype(np.uint32), 2).reshape(-1, 2)
+        allp = np.unique(np.concatenate([pairs, loops]), axis=0)
+        off, nbr = csr(n, allp)
+        g = build(gbg, kind, n, allp)
+        want_ref = ref.csr(n, off, nbr)
+        assert np.array_equal(gbg.kcore(g), want_ref.kcore())
+        assert np.array_equal(gbg.kcore(g), orc.kcore(n, off, nbr))
+        assert np.array_equal(gbg.coloring(g), orc.coloring(n, off, nbr))
+        assert np.array_equal(gbg.mis(g, trial), orc.mis(n, off, nbr, trial))
+        for a, b in zip(gbg.ldd(g, 0.3, trial), want_ref.ldd(0.3, trial)):
+            assert np.array_equal(a, b)

@@ -492,3 +492,20 @@ def test_bytecode_known_answers_and_reference(ref, orc):
         want = ref.csr(n, off, nbr).compressed()
         got = orc.bytecode_encode(n, off, nbr)
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_greedy_consumers_with_self_loops(ref, orc):
+    """Self-loops are legal CsrGraph input (csr.cpp:9-25); kcore counts them
+    in the degree, coloring / mis never let a vertex beat itself."""
+    rng = np.random.default_rng(11)
+    for trial in range(4):
+        n, pairs = ref.er(80, 0.08, 50 + trial)
+        loops = np.repeat(rng.choice(n, 10, replace=False).astype(np.uint32), 2).reshape(-1, 2)
+        allp = np.unique(np.concatenate([pairs, loops]), axis=0)
+        off, nbr = csr(n, allp)
+        g = ref.csr(n, off, nbr)
+        assert np.array_equal(orc.kcore(n, off, nbr), g.kcore())
+        assert np.array_equal(orc.coloring(n, off, nbr), g.coloring())
+        assert np.array_equal(orc.mis(n, off, nbr, trial), g.mis(trial))
+        for a, b in zip(orc.ldd(n, off, nbr, 0.3, trial), g.ldd(0.3, trial)):
+            assert np.array_equal(a, b)
