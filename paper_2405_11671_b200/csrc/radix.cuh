@@ -1,19 +1,23 @@
 // Stable LSD radix sort of uint64 keys over their low `bits` bits, 8-bit
-// digits, three launches per digit pass:
+// digits, one launch per digit pass (the "onesweep" structure):
 //
-//   radix_hist_k     per 4096-key tile: digit histogram -> counts[digit][tile]
-//   device_scan      exclusive scan of the digit-major counts -> global slot
-//                    of (digit, tile)
-//   radix_scatter_k  per tile: stable rank of every key among the tile's keys
-//                    with the same digit (16 rounds of 256 keys; within a
-//                    warp __match_any_sync finds the peers, across warps a
-//                    per-round digit count table), keys staged in shared
-//                    memory in digit order, then written out so that
-//                    consecutive threads store consecutive slots of a digit
-//                    bucket.
+//   radix_global_hist_k  one read of the keys: the histogram of every digit
+//                        pass at once -> the global bucket base of each digit
+//   radix_onesweep_k     per 4096-key tile (tiles taken in order from an
+//                        atomic counter): digit counts of the tile, published
+//                        at once; the tile's exclusive prefix per digit from a
+//                        decoupled look-back over the preceding tiles'
+//                        published counts / prefixes; stable rank of every
+//                        key among the tile's keys with the same digit (within
+//                        a warp __match_any_sync finds the peers, across warps
+//                        per-warp digit counts), keys staged in shared memory
+//                        in digit order, then written so that consecutive
+//                        threads store consecutive slots of a digit bucket.
 //
-// Used by the batch-update "prepare" (batch.cpp:34-42: sort the raw arcs)
-// and the R-MAT generator's normalisation (generators.cpp:22-23).
+// So a pass reads and writes the keys once (the former separate histogram
+// pass and count scan are gone).  Used by the batch-update "prepare"
+// (batch.cpp:34-42: sort the raw arcs) and the R-MAT generator's
+// normalisation (generators.cpp:22-23).
 #pragma once
 
 #include "scan.cuh"
@@ -27,24 +31,44 @@ constexpr int kRadixBits = 8;
 constexpr uint32_t kRadix = 1u << kRadixBits;
 static_assert(kSortThreads == static_cast<int>(kRadix), "one thread per digit in the tile scan");
 
-static __global__ void __launch_bounds__(kSortThreads) radix_hist_k(const uint64_t* __restrict__ keys, uint64_t n, int shift,
-                                                             uint32_t ntiles, uint32_t* __restrict__ counts) {
-  __shared__ uint32_t h[kRadix];
-  for (uint32_t d = threadIdx.x; d < kRadix; d += kSortThreads) h[d] = 0;
+constexpr int kMaxPasses = 8;
+constexpr uint64_t kLbAgg = 1ull << 62;   // published: the tile's own count
+constexpr uint64_t kLbPre = 2ull << 62;   // published: inclusive prefix through the tile
+constexpr uint64_t kLbVal = (1ull << 62) - 1;
+
+static __global__ void __launch_bounds__(kSortThreads) radix_global_hist_k(const uint64_t* __restrict__ keys,
+                                                                           uint64_t n, int passes,
+                                                                           uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kMaxPasses][kRadix];
+  for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kSortTile;
-#pragma unroll 4
-  for (int r = 0; r < kSortRounds; ++r) {
-    const uint64_t i = base + r * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & (kRadix - 1)], 1u);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const uint64_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (p * kRadixBits)) & (kRadix - 1)], 1u);
   }
   __syncthreads();
-  for (uint32_t d = threadIdx.x; d < kRadix; d += kSortThreads) counts[d * ntiles + blockIdx.x] = h[d];
+  for (int p = 0; p < passes; ++p)
+    if (h[p][threadIdx.x]) atomicAdd(hist + p * kRadix + threadIdx.x, h[p][threadIdx.x]);
 }
 
-static __global__ void __launch_bounds__(kSortThreads) radix_scatter_k(const uint64_t* __restrict__ in,
-                                                                uint64_t* __restrict__ out, uint64_t n, int shift,
-                                                                uint32_t ntiles, const uint32_t* __restrict__ offs) {
+// per pass: exclusive scan of the 256 digit counts -> bucket bases (in place)
+static __global__ void __launch_bounds__(kSortThreads) radix_bases_k(uint32_t* hist, int passes) {
+  __shared__ uint32_t s_red[33];
+  for (int p = 0; p < passes; ++p) {
+    uint32_t all;
+    const uint32_t c = hist[p * kRadix + threadIdx.x];
+    const uint32_t e = block_exclusive_scan(c, s_red, all);
+    __syncthreads();
+    hist[p * kRadix + threadIdx.x] = e;
+    __syncthreads();
+  }
+}
+
+static __global__ void __launch_bounds__(kSortThreads) radix_onesweep_k(const uint64_t* __restrict__ in,
+                                                                        uint64_t* __restrict__ out, uint64_t n,
+                                                                        int shift, const uint32_t* __restrict__ base,
+                                                                        uint64_t* state, unsigned int* tile_ctr) {
   constexpr int kWarps = kSortThreads / 32;
   constexpr uint32_t kSub = kSortTile / kWarps;  // 512 consecutive keys per warp
   __shared__ uint64_t s_keys[kSortTile];
@@ -52,18 +76,19 @@ static __global__ void __launch_bounds__(kSortThreads) radix_scatter_k(const uin
   __shared__ uint32_t s_start[kRadix];   // first slot of each digit inside the digit-sorted tile
   __shared__ uint32_t s_cnt[kWarps][kRadix];  // per-warp digit counts, then per-warp running slots
   __shared__ uint32_t s_red[33];
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);  // processing order == tile order
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kSortTile + static_cast<uint64_t>(warp) * kSub;
-  const uint32_t lt = (1u << lane) - 1;
-
   for (uint32_t x = lane; x < kRadix; x += 32) s_cnt[warp][x] = 0;
-  for (uint32_t d = threadIdx.x; d < kRadix; d += kSortThreads) s_base[d] = offs[d * ntiles + blockIdx.x];
-  __syncwarp();
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base0 = static_cast<uint64_t>(tile) * kSortTile + static_cast<uint64_t>(warp) * kSub;
+  const uint32_t lt = (1u << lane) - 1;
   // 1. each warp: its keys (coalesced, kept in registers) and digit counts
   uint64_t k[kSortRounds];
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
-    const uint64_t i = base + r * 32 + lane;
+    const uint64_t i = base0 + r * 32 + lane;
     const bool valid = i < n;
     k[r] = valid ? in[i] : ~0ull;
     const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
@@ -72,12 +97,18 @@ static __global__ void __launch_bounds__(kSortThreads) radix_scatter_k(const uin
     __syncwarp();
   }
   __syncthreads();
-  // 2. digit totals -> tile start of each digit; per-warp start inside it
+  // 2. digit totals: publish them, tile start of each digit, per-warp starts
   {
     const uint32_t d = threadIdx.x;  // kSortThreads == kRadix
     uint32_t tot = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) tot += s_cnt[w][d];
+    volatile uint64_t* st = state + static_cast<uint64_t>(tile) * kRadix + d;
+    if (tile == 0) {
+      *st = kLbPre | tot;
+    } else {
+      *st = kLbAgg | tot;
+    }
     uint32_t all;
     const uint32_t start = block_exclusive_scan(tot, s_red, all);
     s_start[d] = start;
@@ -88,12 +119,24 @@ static __global__ void __launch_bounds__(kSortThreads) radix_scatter_k(const uin
       s_cnt[w][d] = run;
       run += c;
     }
+    // 3. decoupled look-back: the tile's exclusive prefix of digit d
+    uint64_t excl = 0;
+    for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0; --t) {
+      const volatile uint64_t* q = state + static_cast<uint64_t>(t) * kRadix + d;
+      uint64_t v;
+      while (((v = *q) >> 62) == 0) {
+      }
+      excl += v & kLbVal;
+      if ((v >> 62) == 2) break;
+    }
+    if (tile > 0) *st = kLbPre | (excl + tot);
+    s_base[d] = base[d] + static_cast<uint32_t>(excl);
   }
   __syncthreads();
-  // 3. each warp ranks its keys in order (stable) into the staged tile
+  // 4. each warp ranks its keys in order (stable) into the staged tile
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
-    const bool valid = base + r * 32 + lane < n;
+    const bool valid = base0 + r * 32 + lane < n;
     const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     if (valid) s_keys[s_cnt[warp][d] + __popc(peers & lt)] = k[r];
@@ -102,9 +145,9 @@ static __global__ void __launch_bounds__(kSortThreads) radix_scatter_k(const uin
     __syncwarp();
   }
   __syncthreads();
-  // 4. coalesced write-out: slot j of the digit-sorted tile goes to
+  // 5. coalesced write-out: slot j of the digit-sorted tile goes to
   // s_base[digit] + (j - s_start[digit])
-  const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSortTile;
+  const uint64_t tile0 = static_cast<uint64_t>(tile) * kSortTile;
   const uint32_t len = static_cast<uint32_t>(n - tile0 < kSortTile ? n - tile0 : kSortTile);
   for (uint32_t j = threadIdx.x; j < len; j += kSortThreads) {
     const uint64_t key = s_keys[j];
@@ -119,16 +162,24 @@ inline uint64_t* radix_sort_u64(gbg_graph* g, uint64_t* keys, uint64_t* scratch,
                                 const char* tag) {
   if (n <= 1 || bits <= 0) return keys;
   if (n > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "radix sort: more than 2^32-1 keys");
+  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+  if (passes > kMaxPasses) fail(GBG_ERR_LOGIC, "radix sort: too many digit passes");
   const uint32_t ntiles = static_cast<uint32_t>((n + kSortTile - 1) / kSortTile);
-  const uint64_t ncounts = static_cast<uint64_t>(ntiles) * kRadix;
-  uint32_t* counts = g->ws.get<uint32_t>(std::string(tag) + ".cnt", ncounts + 1);
+  const std::string t(tag);
+  uint32_t* hist = g->ws.get<uint32_t>(t + ".hist", kMaxPasses * kRadix);
+  uint64_t* state = g->ws.get<uint64_t>(t + ".lb", static_cast<uint64_t>(ntiles) * kRadix);
+  unsigned int* ctr = g->ws.get<unsigned int>(t + ".ctr", kMaxPasses);
+  GBG_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), g->stream));
+  GBG_CUDA(cudaMemsetAsync(ctr, 0, kMaxPasses * sizeof(unsigned int), g->stream));
+  GBG_LAUNCH(g, radix_global_hist_k, grid_for(n, kSortThreads, static_cast<unsigned>(g->sm_count) * 4u),
+             kSortThreads, 0, keys, n, passes, hist);
+  GBG_LAUNCH(g, radix_bases_k, 1, kSortThreads, 0, hist, passes);
   uint64_t* src = keys;
   uint64_t* dst = scratch;
-  for (int shift = 0; shift < bits; shift += kRadixBits) {
-    GBG_LAUNCH(g, radix_hist_k, ntiles, kSortThreads, 0, src, n, shift, ntiles, counts);
-    device_scan<uint32_t>(g, ArrayIn<uint32_t>{counts}, ArrayOut<uint32_t>{counts}, ncounts, counts + ncounts,
-                          (std::string(tag) + ".scan").c_str());
-    GBG_LAUNCH(g, radix_scatter_k, ntiles, kSortThreads, 0, src, dst, n, shift, ntiles, counts);
+  for (int p = 0; p < passes; ++p) {
+    GBG_CUDA(cudaMemsetAsync(state, 0, static_cast<uint64_t>(ntiles) * kRadix * sizeof(uint64_t), g->stream));
+    GBG_LAUNCH(g, radix_onesweep_k, ntiles, kSortThreads, 0, src, dst, n, p * kRadixBits, hist + p * kRadix, state,
+               ctr + p);
     std::swap(src, dst);
   }
   return src;

@@ -205,9 +205,9 @@ class _Graph:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _L is not None:  # module globals may be gone at interpreter exit
             _L.gbg_graph_destroy(h)
-            self._h = None
+        self._h = None
 
     def __enter__(self):
         return self
