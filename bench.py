@@ -480,8 +480,18 @@ def main():
         # configs[4]: updates on the blocked container at s22
         upd, _gb = run_updates(torch, gbg, 22, max(1, min(args.steps, 3)), 1, [10**4, 10**5, 10**6, 10**7])
         workloads["updates_s22"] = upd
-        log("secondary workloads done")
         del _gb
+        # capacity: the same PageRank at scale 26 (67M vertices, 2.1G arcs,
+        # ~42 GB resident with the generator's buffers) on the one GPU
+        t0 = time.perf_counter()
+        g26 = gbg.generate_rmat(26, 16 << 26, 1, *RMAT)
+        gen26 = time.perf_counter() - t0
+        m26 = g26.num_edges()
+        t26, _, _ = run_pagerank(torch, gbg, g26, max(1, min(args.steps, 2)), 1)
+        workloads["pr_s26"] = {"gteps": 20 * m26 / t26 / 1e9, "ms": t26 * 1e3, "m": m26,
+                               "generate_s": gen26, "note": "capacity run, not a BASELINE config"}
+        del g26
+        log("secondary workloads done")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
