@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
       if (tid == 0) s.dscan[cur][size] = degsum;  // sentinel closing the last segment
       for (uint64_t w = tid; w < s.nw; w += nthreads) s.bm[nxt][w] = 0;
       grid.sync();
-      const uint64_t tiles = (degsum + kPushTile - 1) / kPushTile;
+      const uint32_t ipt = push_ipt(degsum, gridDim.x);
+      const uint64_t tiles = push_tiles(degsum, ipt);
       for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         push_tile(g, s.list[cur], static_cast<uint32_t>(size), s.dscan[cur], degsum, op, s.list[nxt], s.dscan[nxt],
-                  s.bm[nxt], acc, t, s_idx);
+                  s.bm[nxt], acc, t, s_idx, ipt);
         __syncthreads();
       }
     }
@@ -282,9 +283,10 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
       g->hscalar[4] = cur.degsum;
       GBG_CUDA(cudaMemcpyAsync(cur.dscan + cur.size, g->hscalar + 4, sizeof(uint64_t), cudaMemcpyHostToDevice,
                                g->stream));
-      const uint64_t tiles = (cur.degsum + kPushTile - 1) / kPushTile;
-      GBG_LAUNCH(g, (push_k<G, Op>), static_cast<unsigned>(tiles), kPushThreads, 0, view, cur.list,
-                 static_cast<uint32_t>(cur.size), cur.dscan, cur.degsum, op, out.list, out.dscan, out.bm, tb.packed);
+      const uint32_t ipt = push_ipt(cur.degsum, static_cast<uint64_t>(g->sm_count) * kPushCtasPerSm);
+      GBG_LAUNCH(g, (push_k<G, Op>), static_cast<unsigned>(push_tiles(cur.degsum, ipt)), kPushThreads, 0, view,
+                 cur.list, static_cast<uint32_t>(cur.size), cur.dscan, cur.degsum, op, out.list, out.dscan, out.bm,
+                 tb.packed, ipt);
     }
     out.has_list = out.has_bm = true;
   }

@@ -215,9 +215,9 @@ void cc_run(gbg_graph* g, uint32_t* labels_dev) {
       if (E) {
         unsigned long long* counters = g->ws.get<unsigned long long>("cc.counters", 2);
         GBG_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), g->stream));
-        const uint64_t tiles = (E + kPushTile - 1) / kPushTile;
-        GBG_LAUNCH(g, (push_k<G, RestOp>), static_cast<unsigned>(tiles), kPushThreads, 0, view, list, k, dscan, E,
-                   RestOp{parent}, list, nullptr, nullptr, counters);
+        const uint32_t ipt = push_ipt(E, static_cast<uint64_t>(g->sm_count) * kPushCtasPerSm);
+        GBG_LAUNCH(g, (push_k<G, RestOp>), static_cast<unsigned>(push_tiles(E, ipt)), kPushThreads, 0, view, list,
+                   k, dscan, E, RestOp{parent}, list, nullptr, nullptr, counters, ipt);
       }
     }
   });

@@ -158,8 +158,9 @@ __device__ __forceinline__ bool color_light(uint32_t v, const uint64_t* __restri
   const uint64_t b = boff[v], d = boff[v + 1] - b;
   if (d >= kLightBeaters) return false;
   uint64_t used = 0;
+#pragma unroll 4
   for (uint32_t j = 0; j < d; ++j) {
-    const uint32_t c = colors[bnbr[b + j]];
+    const uint32_t c = __ldcg(colors + bnbr[b + j]);  // coloured by other CTAs in earlier rounds
     if (c < 64) used |= uint64_t{1} << c;
   }
   colors[v] = static_cast<uint32_t>(__ffsll(static_cast<long long>(~used)) - 1);
@@ -221,11 +222,37 @@ __global__ void __launch_bounds__(kColorThreads)
   for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) color_heavy(heavy[h], boff, bnbr, colors, s_bm, &s_first);
 }
 
+// Release with colouring on emission: the lane whose decrement makes v
+// ready colours it at once when it has < 64 beaters (all coloured in
+// earlier rounds: a beater is coloured before it releases), so the next
+// round only releases; heavier vertices are queued for a CTA-wide colouring
+// step after the round's barrier.
+struct ColorReleaseFusedOp {
+  LlfBeats beats;
+  uint32_t* waiting;
+  const uint64_t* boff;
+  const uint32_t* bnbr;
+  uint32_t* colors;
+  uint32_t* heavy;
+  uint32_t* nheavy;
+  __device__ __forceinline__ bool cond(uint32_t) const { return true; }
+  __device__ __forceinline__ bool claim(uint32_t) const { return true; }
+  __device__ __forceinline__ bool update(uint32_t u, uint32_t v) const {
+    if (beats(v, u) || atomicSub(waiting + v, 1u) != 1u) return false;
+    if (color_light(v, boff, bnbr, colors)) return true;
+    heavy[atomicAdd(nheavy, 1u)] = v;
+    return false;
+  }
+  __device__ __forceinline__ void dense_word(uint64_t, uint32_t) const {}
+};
+
 // All rounds in one persistent cooperative launch (the BFS pattern,
-// bfs.cu): per round, lanes colour the light ready vertices and queue the
-// heavy ones; CTAs colour the heavy ones; the release push emits the next
-// ready list; grid barriers separate the steps instead of host round trips.
-// Counters rotate through a ring of three (reset two rounds after use).
+// bfs.cu): per round, the release push over the vertices coloured last
+// round colours the light vertices it makes ready and emits them as the
+// next list; after a grid barrier, CTAs colour the heavy ones and append
+// them to the same list (a second barrier only in rounds that have heavy
+// vertices).  Counters rotate through a ring of three (reset two rounds
+// after use).
 struct ColorCoop {
   uint32_t* list[2];
   uint64_t* dscan[2];
@@ -235,9 +262,17 @@ struct ColorCoop {
   const uint64_t* boff;
   const uint32_t* bnbr;
   uint32_t* colors;
-  ColorReleaseOp rel;
-  unsigned long long* rounds;  // [0] rounds, [1..3] ns in the light / heavy / release steps (CTA 0)
+  LlfBeats beats;
+  uint32_t* waiting;
+  unsigned long long* rounds;  // [0] rounds, [1] ns in releases, [2] ns in heavy steps (CTA 0)
 };
+
+// the initially ready vertices have no beaters: colour 0 (first fit)
+__global__ void color_zero_k(const uint32_t* list, const unsigned long long* packed, uint32_t* colors) {
+  const uint64_t k = pack_count(*packed);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += stride) colors[list[i]] = 0;
+}
 
 template <class G>
 __global__ void __launch_bounds__(kPushThreads, 4) color_coop_k(G g, ColorCoop s) {
@@ -246,10 +281,9 @@ __global__ void __launch_bounds__(kPushThreads, 4) color_coop_k(G g, ColorCoop s
   __shared__ uint32_t s_bm[kHeavyWindow / 32];
   __shared__ uint32_t s_first;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   int cur = 0;
   uint64_t r = 0;
-  unsigned long long t_light = 0, t_heavy = 0, t_rel = 0, t0 = globaltimer_ns();
+  unsigned long long t_rel = 0, t_heavy = 0, t0 = globaltimer_ns();
   for (;; ++r) {
     const unsigned long long p = *reinterpret_cast<volatile unsigned long long*>(s.packed + r % 3);
     const uint64_t size = pack_count(p), degsum = pack_degsum(p);
@@ -259,39 +293,43 @@ __global__ void __launch_bounds__(kPushThreads, 4) color_coop_k(G g, ColorCoop s
       s.nheavy[(r + 1) % 3] = 0;
     }
     uint32_t* nh_ctr = s.nheavy + r % 3;
-    for (uint64_t i = tid; i < size; i += nthreads) {
-      const uint32_t v = s.list[cur][i];
-      if (!color_light(v, s.boff, s.bnbr, s.colors)) s.heavy[atomicAdd(nh_ctr, 1u)] = v;
-    }
-    grid.sync();
-    unsigned long long t1 = globaltimer_ns();
-    t_light += t1 - t0;
-    const uint32_t nh = *reinterpret_cast<volatile uint32_t*>(nh_ctr);
-    if (nh) {
-      for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x)
-        color_heavy(s.heavy[h], s.boff, s.bnbr, s.colors, s_bm, &s_first);
-      grid.sync();
-      t0 = globaltimer_ns();
-      t_heavy += t0 - t1;
-      t1 = t0;
-    }
+    unsigned long long* next_ctr = s.packed + (r + 1) % 3;
     const int nxt = cur ^ 1;
-    const uint64_t tiles = (degsum + kPushTile - 1) / kPushTile;
+    const ColorReleaseFusedOp op{s.beats, s.waiting, s.boff, s.bnbr, s.colors, s.heavy, nh_ctr};
+    const uint32_t ipt = push_ipt(degsum, gridDim.x);
+    const uint64_t tiles = push_tiles(degsum, ipt);
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      push_tile(g, s.list[cur], static_cast<uint32_t>(size), s.dscan[cur], degsum, s.rel, s.list[nxt], s.dscan[nxt],
-                static_cast<uint32_t*>(nullptr), s.packed + (r + 1) % 3, t, s_idx);
+      push_tile(g, s.list[cur], static_cast<uint32_t>(size), s.dscan[cur], degsum, op, s.list[nxt], s.dscan[nxt],
+                static_cast<uint32_t*>(nullptr), next_ctr, t, s_idx, ipt);
       __syncthreads();
     }
     grid.sync();
-    t0 = globaltimer_ns();
-    t_rel += t0 - t1;
+    unsigned long long t1 = globaltimer_ns();
+    t_rel += t1 - t0;
+    t0 = t1;
+    const uint32_t nh = *reinterpret_cast<volatile uint32_t*>(nh_ctr);
+    if (nh) {
+      for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const uint32_t v = s.heavy[h];
+        color_heavy(v, s.boff, s.bnbr, s.colors, s_bm, &s_first);
+        if (threadIdx.x == 0) {
+          const uint64_t dv = g.degree(v);
+          const unsigned long long old = atomicAdd(next_ctr, (1ull << kPackShift) | dv);
+          s.list[nxt][pack_count(old)] = v;
+          s.dscan[nxt][pack_count(old)] = pack_degsum(old);
+        }
+      }
+      grid.sync();
+      t1 = globaltimer_ns();
+      t_heavy += t1 - t0;
+      t0 = t1;
+    }
     cur = nxt;
   }
   if (tid == 0) {
     s.rounds[0] = r;
-    s.rounds[1] = t_light;
+    s.rounds[1] = t_rel;
     s.rounds[2] = t_heavy;
-    s.rounds[3] = t_rel;
   }
 }
 
@@ -385,18 +423,20 @@ void coloring_run(gbg_graph* g, G view, uint32_t* colors) {
   GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, color_coop_k<G>, kPushThreads, 0));
   uint64_t rounds = 0;
   if (coop && per_sm > 0) {
-    ColorCoop cs{{L.id[0], L.id[1]}, {L.dscan[0], L.dscan[1]}, sc, nheavy, heavy, boff, bnbr, colors, rel, sc + 3};
+    GBG_LAUNCH(g, color_zero_k, grid_for(n, 256), 256, 0, L.id[0], sc, colors);
+    ColorCoop cs{{L.id[0], L.id[1]}, {L.dscan[0], L.dscan[1]}, sc, nheavy, heavy, boff, bnbr, colors, beats, waiting,
+                 sc + 3};
     void* args[] = {&view, &cs};
     GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(color_coop_k<G>),
                                          static_cast<unsigned>(per_sm * g->sm_count), kPushThreads, args, 0,
                                          g->stream));
     g->launches++;
     if (PhaseTrace::enabled()) {
-      unsigned long long h[4];
+      unsigned long long h[3];
       read_scalars(g, sc + 3, sizeof(h), h);
       rounds = h[0];
-      std::fprintf(stderr, "[gbg] coloring steps (CTA 0): light %.2f ms, heavy %.2f ms, release %.2f ms\n", h[1] * 1e-6,
-                   h[2] * 1e-6, h[3] * 1e-6);
+      std::fprintf(stderr, "[gbg] coloring: %llu rounds (cooperative): releases %.2f ms, heavy steps %.2f ms\n",
+                   h[0], h[1] * 1e-6, h[2] * 1e-6);
     }
   } else {
     unsigned long long p = 0;

@@ -179,10 +179,11 @@ __global__ void __launch_bounds__(kPushThreads, 4) kcore_coop_k(G g, KcoreCoop s
       const uint64_t size = pack_count(p), degsum = pack_degsum(p);
       c = s.slot + (step % 3) * kSlot;
       if (t0) reset_slot(s.slot + ((step + 1) % 3) * kSlot);
-      const uint64_t tiles = (degsum + kPushTile - 1) / kPushTile;
+      const uint32_t ipt = push_ipt(degsum, gridDim.x);
+      const uint64_t tiles = push_tiles(degsum, ipt);
       for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         push_tile(g, s.list[cf], static_cast<uint32_t>(size), s.dscan[cf], degsum, op, s.list[cf ^ 1],
-                  s.dscan[cf ^ 1], static_cast<uint32_t*>(nullptr), c, t, s_idx);
+                  s.dscan[cf ^ 1], static_cast<uint32_t*>(nullptr), c, t, s_idx, ipt);
         __syncthreads();
       }
       grid.sync();

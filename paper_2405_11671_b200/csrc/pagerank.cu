@@ -48,16 +48,18 @@ constexpr uint32_t kL1Hot = 16384;
 // Degree classes over the degree-descending rows: class c gives each row
 // T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
 // at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
-// 4096) splits rows into kChunk-edge chunks across CTAs; classes 1-3 (513
-// to 4096) take a warp per row in 512-edge passes (no block barrier); the
-// last class is the isolated rows (finalize only).
+// 4096) splits rows into kChunk-edge chunks across CTAs; classes 1-2 (1025
+// to 4096) take a CTA per row; class 3 (513 to 1024) a warp per row in two
+// 512-edge passes (no block barrier: better at scale 24, while the CTA form
+// stays better for the longer rows, which dominate at scale 20); the last
+// class is the isolated rows (finalize only).
 constexpr int kClasses = 15;
 __host__ __device__ constexpr uint32_t class_threads(int c) {
-  constexpr uint32_t t[kClasses] = {256, 32, 32, 32, 32, 32, 32, 16, 8, 4, 2, 1, 1, 1, 1};
+  constexpr uint32_t t[kClasses] = {256, 256, 256, 32, 32, 32, 32, 16, 8, 4, 2, 1, 1, 1, 1};
   return t[c];
 }
 __host__ __device__ constexpr uint32_t class_k(int c) {
-  constexpr uint32_t k[kClasses] = {16, 128, 64, 32, 16, 8, 4, 4, 4, 4, 4, 4, 2, 1, 0};
+  constexpr uint32_t k[kClasses] = {16, 16, 8, 32, 16, 8, 4, 4, 4, 4, 4, 4, 2, 1, 0};
   return k[c];
 }
 __host__ __device__ constexpr uint32_t class_max_deg(int c) { return c == 0 ? 0xffffffffu : class_threads(c) * class_k(c); }
@@ -352,6 +354,16 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
         a.heavy_counter[r] = 0;
       }
       __syncthreads();
+    } else if (class_threads(c) == kPrThreads) {
+      // ---- one CTA per row
+      const uint32_t r = a.row_begin[c] + static_cast<uint32_t>(w - a.unit_begin[c]);
+      const uint64_t rb = __ldg(a.off + r), d = __ldg(a.off + r + 1) - rb;
+      double p;
+      if (class_k(c) == 16) p = gather_sum<16>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      else if (class_k(c) == 8) p = gather_sum<8>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      else p = gather_sum<4>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
+      const double s = block_sum(p, s_red);
+      if (threadIdx.x == 0) pr_finalize(a, base, r, d, s, err, dang);
     } else {
       // ---- a fixed group of lanes per row, rows of the unit consecutive
       const uint32_t lanes = class_threads(c);
@@ -366,8 +378,6 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
         const uint64_t rb = ld_stream_u64(a.off + r, pf);
         d = ld_stream_u64(a.off + r + 1, pf) - rb;
         switch (class_k(c)) {
-          case 128:
-          case 64:
           case 32:  // warp per row, 512 edges per pass (no block barrier)
             for (uint64_t o = 0; o < d; o += 16 * 32) acc += gather_sum<16>(a, rb + o, d - o, l, 32, pf, pl);
             break;

@@ -121,15 +121,32 @@ struct FrontierDegIn {
 // Frontier data (list, prefix, bitmaps) may have been written earlier in
 // the same launch by the persistent BFS kernel, so it is read with plain
 // (coherent) loads; only the graph itself goes through the read-only path.
+// Edges per thread (tile = kPushThreads * ipt edges): the full kPushIPT
+// when the frontier's edges fill the grid, fewer when they do not — a
+// thread walks its edges one dependent chain after another, so a small
+// frontier on large tiles would leave most of the grid idle while a few
+// CTAs walk 8 chains each.
+__host__ __device__ __forceinline__ uint32_t push_ipt(uint64_t E, uint64_t ctas) {
+  const uint64_t per = (E + ctas * kPushThreads - 1) / (ctas * kPushThreads);
+  return per < 1 ? 1u : (per > static_cast<uint64_t>(kPushIPT) ? static_cast<uint32_t>(kPushIPT) : static_cast<uint32_t>(per));
+}
+__host__ __device__ __forceinline__ uint64_t push_tiles(uint64_t E, uint32_t ipt) {
+  return (E + static_cast<uint64_t>(kPushThreads) * ipt - 1) / (static_cast<uint64_t>(kPushThreads) * ipt);
+}
+// resident CTAs a one-shot push launch can count on (8 per SM)
+constexpr uint64_t kPushCtasPerSm = 8;
+
 template <class G, class Op>
 __device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, const uint64_t* dscan, uint64_t E,
                                           Op op, uint32_t* out, uint64_t* out_dscan, uint32_t* out_bm,
-                                          unsigned long long* packed, uint64_t tile, uint32_t* s_idx) {
-  const uint64_t e0 = tile * kPushTile;
+                                          unsigned long long* packed, uint64_t tile, uint32_t* s_idx,
+                                          uint32_t ipt = kPushIPT) {
+  const uint32_t tile_len = kPushThreads * ipt;
+  const uint64_t e0 = tile * tile_len;
   if (e0 >= E) return;
-  const uint32_t len = static_cast<uint32_t>(E - e0 < kPushTile ? E - e0 : kPushTile);
+  const uint32_t len = static_cast<uint32_t>(E - e0 < tile_len ? E - e0 : tile_len);
   {
-    const uint32_t k0 = threadIdx.x * kPushIPT;
+    const uint32_t k0 = threadIdx.x * ipt;
     if (k0 < len) {
       const uint64_t e = e0 + k0;
       uint32_t lo = 0, hi = nf;  // dscan[lo] <= e < dscan[hi]
@@ -141,7 +158,7 @@ __device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, c
       uint64_t next = i + 1 < nf ? dscan[i + 1] : E;
 #pragma unroll
       for (int j = 0; j < kPushIPT; ++j) {
-        if (k0 + j >= len) break;
+        if (j >= static_cast<int>(ipt) || k0 + j >= len) break;
         while (next <= e + j) {
           ++i;
           next = i + 1 < nf ? dscan[i + 1] : E;
@@ -198,9 +215,9 @@ template <class G, class Op>
 __global__ void __launch_bounds__(kPushThreads)
     push_k(G g, const uint32_t* __restrict__ F, uint32_t nf, const uint64_t* __restrict__ dscan,
            uint64_t E, Op op, uint32_t* __restrict__ out, uint64_t* __restrict__ out_dscan,
-           uint32_t* __restrict__ out_bm, unsigned long long* packed) {
+           uint32_t* __restrict__ out_bm, unsigned long long* packed, uint32_t ipt) {
   __shared__ uint32_t s_idx[kPushTile];
-  push_tile(g, F, nf, dscan, E, op, out, out_dscan, out_bm, packed, blockIdx.x, s_idx);
+  push_tile(g, F, nf, dscan, E, op, out, out_dscan, out_bm, packed, blockIdx.x, s_idx, ipt);
 }
 
 // one push over a frontier list with its degree prefix (E = total degree)
@@ -208,9 +225,9 @@ template <class G, class Op>
 inline void push_list(gbg_graph* g, G view, const uint32_t* F, uint64_t nf, const uint64_t* dscan, uint64_t E, Op op,
                       uint32_t* out, uint64_t* out_dscan, unsigned long long* packed) {
   if (!nf || !E) return;
-  const uint64_t tiles = (E + kPushTile - 1) / kPushTile;
-  GBG_LAUNCH(g, (push_k<G, Op>), static_cast<unsigned>(tiles), kPushThreads, 0, view, F, static_cast<uint32_t>(nf),
-             dscan, E, op, out, out_dscan, nullptr, packed);
+  const uint32_t ipt = push_ipt(E, static_cast<uint64_t>(g->sm_count) * kPushCtasPerSm);
+  GBG_LAUNCH(g, (push_k<G, Op>), static_cast<unsigned>(push_tiles(E, ipt)), kPushThreads, 0, view, F,
+             static_cast<uint32_t>(nf), dscan, E, op, out, out_dscan, nullptr, packed, ipt);
 }
 
 // Select the vertices with pred(v) into an ascending-by-warp id list with
