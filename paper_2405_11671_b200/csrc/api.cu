@@ -154,6 +154,7 @@ gbg_graph::~gbg_graph() {
   dfree(bcap);
   dfree(pool);
   dfree(voff);
+  dfree(first);
   dfree(coff);
   dfree(cbytes);
   dfree(cdeg);

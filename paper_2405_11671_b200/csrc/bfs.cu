@@ -95,6 +95,7 @@ struct CoopState {
   uint64_t nw;
   double threshold;            // (1/20) * m, evaluated on the host like traversal.cpp:105-106
   uint32_t src;
+  const uint32_t* first;       // first neighbours (dense-level shortcut)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     BfsOp op{s.visited, s.depth, level};
     unsigned long long* acc = s.packed + level % 3;
     if (dense) {
-      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc);
+      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc, s.first);
       has_list = false;
     } else {
       if (!has_list) {
@@ -273,7 +274,7 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
       cur.has_bm = true;
     }
     GBG_LAUNCH(g, (pull_k<G, Op, kEarly>), pull_grid(g, tb.nw), kPullThreads, 0, view, cur.bm, op, out.bm, tb.nw,
-               tb.packed);
+               tb.packed, kEarly ? first_neighbors(g) : static_cast<const uint32_t*>(nullptr));
     out.has_bm = true;
   } else {
     ensure_list(g, view, tb, cur);
@@ -291,6 +292,17 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
     out.has_list = out.has_bm = true;
   }
   read_packed(g, tb.packed, out);
+}
+
+template <class G>
+__global__ void first_nbr_k(G g, uint32_t* first) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.n; v += stride) {
+    uint64_t b;
+    uint32_t d;
+    g.seg(static_cast<uint32_t>(v), b, d);
+    first[v] = d ? g.at(b) : kNoFirst;
+  }
 }
 
 // The persistent path; false when the device cannot co-schedule the grid.
@@ -322,6 +334,7 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.nw = tb.nw;
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
   s.src = src;
+  s.first = first_neighbors(g);
   void* args[] = {&view, &s};
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));
@@ -478,6 +491,19 @@ void bc_run(gbg_graph* g, G view, uint32_t src, double* delta) {
 }
 
 }  // namespace
+}  // namespace gbg
+
+namespace gbg {
+const uint32_t* first_neighbors(gbg_graph* g) {
+  if (!g->first) g->first = dalloc<uint32_t>(g->n ? g->n : 1);
+  if (!g->first_valid) {
+    with_view(g, [&](auto view) {
+      GBG_LAUNCH(g, first_nbr_k<decltype(view)>, grid_for(g->n, 256), 256, 0, view, g->first);
+    });
+    g->first_valid = true;
+  }
+  return g->first;
+}
 }  // namespace gbg
 
 using namespace gbg;

@@ -188,6 +188,8 @@ struct gbg_graph {
   // derived, rebuilt lazily after updates
   uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
   bool voff_valid = false;
+  uint32_t* first = nullptr;   // first neighbour of every vertex (kNoFirst if isolated), for dense pulls
+  bool first_valid = false;
   gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
 
   gbg::Workspace ws;
@@ -240,6 +242,10 @@ void with_view(gbg_graph* g, F&& f) {
 // Ensure the blocked container's virtual offsets (scan of degrees) are
 // current; returns a pointer usable as CSR-like offsets for scheduling.
 const uint64_t* virtual_offsets(gbg_graph* g);
+
+// Every vertex's first neighbour (traverse.cuh kNoFirst when isolated),
+// kept until the next update (bfs.cu).
+const uint32_t* first_neighbors(gbg_graph* g);
 
 // Every arc has its reverse (checked once per graph version, cc.cu).
 bool graph_is_symmetric(gbg_graph* g);

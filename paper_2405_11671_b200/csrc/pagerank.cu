@@ -531,6 +531,7 @@ void gbg_graph::invalidate_derived() {
   delete pr;
   pr = nullptr;
   voff_valid = false;
+  first_valid = false;
 }
 
 using namespace gbg;
