@@ -96,6 +96,7 @@ struct CoopState {
   double threshold;            // (1/20) * m, evaluated on the host like traversal.cpp:105-106
   uint32_t src;
   const uint32_t* first;       // first neighbours (dense-level shortcut)
+  const uint32_t* iso;         // isolated vertices: pre-set in `visited` (never reached, never pulled)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
   const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = tid; i < g.n; i += nthreads) s.depth[i] = -1;
   for (uint64_t w = tid; w < s.nw; w += nthreads) {
-    s.visited[w] = 0;
+    s.visited[w] = s.iso[w];
     s.bm[0][w] = 0;
   }
   if (tid < 3) s.packed[tid] = 0;
@@ -294,14 +295,23 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
   read_packed(g, tb.packed, out);
 }
 
+// first neighbour of every vertex, and the bitmap of isolated vertices
 template <class G>
-__global__ void first_nbr_k(G g, uint32_t* first) {
+__global__ void first_nbr_k(G g, uint32_t* first, uint32_t* iso) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.n; v += stride) {
-    uint64_t b;
-    uint32_t d;
-    g.seg(static_cast<uint32_t>(v), b, d);
-    first[v] = d ? g.at(b) : kNoFirst;
+  for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~uint64_t{31}; base < g.n;
+       base += stride) {
+    const uint64_t v = base + (threadIdx.x & 31);
+    bool isolated = false;
+    if (v < g.n) {
+      uint64_t b;
+      uint32_t d;
+      g.seg(static_cast<uint32_t>(v), b, d);
+      first[v] = d ? g.at(b) : kNoFirst;
+      isolated = d == 0;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, isolated);
+    if ((threadIdx.x & 31) == 0) iso[base >> 5] = m;
   }
 }
 
@@ -335,6 +345,7 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
   s.src = src;
   s.first = first_neighbors(g);
+  s.iso = isolated_bitmap(g);
   void* args[] = {&view, &s};
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));
@@ -365,7 +376,8 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   TraversalBuffers tb(g);
   uint32_t* visited = g->ws.get<uint32_t>("bfs.visited", tb.nw + 2);
   GBG_CUDA(cudaMemsetAsync(depth, 0xff, g->n * sizeof(int32_t), g->stream));
-  GBG_CUDA(cudaMemsetAsync(visited, 0, tb.nw * sizeof(uint32_t), g->stream));
+  GBG_CUDA(cudaMemcpyAsync(visited, isolated_bitmap(g), tb.nw * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                           g->stream));
   GBG_CUDA(cudaMemsetAsync(tb.a.bm, 0, tb.nw * sizeof(uint32_t), g->stream));
   GBG_LAUNCH(g, bfs_init_k<G>, 1, 1, 0, view, src, visited, depth, tb.a.list, tb.a.dscan, tb.a.bm, tb.packed);
   Frontier* cur = &tb.a;
@@ -495,15 +507,17 @@ void bc_run(gbg_graph* g, G view, uint32_t src, double* delta) {
 
 namespace gbg {
 const uint32_t* first_neighbors(gbg_graph* g) {
-  if (!g->first) g->first = dalloc<uint32_t>(g->n ? g->n : 1);
+  const uint64_t nw = (g->n + 31) / 32;
+  if (!g->first) g->first = dalloc<uint32_t>(g->n + nw + 1);  // ids, then the isolated bitmap
   if (!g->first_valid) {
     with_view(g, [&](auto view) {
-      GBG_LAUNCH(g, first_nbr_k<decltype(view)>, grid_for(g->n, 256), 256, 0, view, g->first);
+      GBG_LAUNCH(g, first_nbr_k<decltype(view)>, grid_for(nw * 32, 256), 256, 0, view, g->first, g->first + g->n);
     });
     g->first_valid = true;
   }
   return g->first;
 }
+const uint32_t* isolated_bitmap(gbg_graph* g) { return first_neighbors(g) + g->n; }
 }  // namespace gbg
 
 using namespace gbg;

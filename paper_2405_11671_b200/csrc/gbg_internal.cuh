@@ -188,7 +188,7 @@ struct gbg_graph {
   // derived, rebuilt lazily after updates
   uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
   bool voff_valid = false;
-  uint32_t* first = nullptr;   // first neighbour of every vertex (kNoFirst if isolated), for dense pulls
+  uint32_t* first = nullptr;   // first neighbour of every vertex (kNoFirst if isolated) + isolated bitmap
   bool first_valid = false;
   gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
 
@@ -246,6 +246,8 @@ const uint64_t* virtual_offsets(gbg_graph* g);
 // Every vertex's first neighbour (traverse.cuh kNoFirst when isolated),
 // kept until the next update (bfs.cu).
 const uint32_t* first_neighbors(gbg_graph* g);
+// Bit v set when v has no neighbours (same lifetime as first_neighbors).
+const uint32_t* isolated_bitmap(gbg_graph* g);
 
 // Every arc has its reverse (checked once per graph version, cc.cu).
 bool graph_is_symmetric(gbg_graph* g);
