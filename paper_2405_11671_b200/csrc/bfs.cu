@@ -12,6 +12,7 @@
 // sparse transition compacts a bitmap (one ordered scan).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -322,7 +323,11 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   GBG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device));
   int per_sm = 0;
   GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_coop_k<G>, kPushThreads, 0));
-  if (!coop || per_sm < 1) return false;
+  static const bool disabled = [] {
+    const char* e = std::getenv("GBG_BFS_COOP");
+    return e && e[0] == '0';
+  }();
+  if (!coop || per_sm < 1 || disabled) return false;
   const unsigned grid = static_cast<unsigned>(per_sm * g->sm_count);
   TraversalBuffers tb(g);
   CoopState s;
