@@ -152,3 +152,36 @@ def test_pipelined_create_with_pagerank_layout(gbg, ref, orc):
     boff[3] = boff[4] + 1
     with pytest.raises(gbg.FormatError):
         gbg.CsrGraph.from_csr(boff, nbr, prepare_pagerank=True)
+
+
+def test_bfs_launch_per_level_path_matches_oracle(gbg, orc, tmp_path):
+    """The launch-per-level BFS (used when cooperative launch is unavailable,
+    forced here with GBG_BFS_COOP=0 in a fresh process) gives the same
+    depths and direction trace as the oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, json; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_2405_11671_b200.graph as gbg\n"
+        "from oracle.bindings import RMAT_A, RMAT_B, RMAT_C\n"
+        "g = gbg.generate_rmat(13, 16 << 13, 1, RMAT_A, RMAT_B, RMAT_C)\n"
+        "b = gbg.BlockedGraph.from_csr_graph(g)\n"
+        "out = {}\n"
+        "for name, h in (('csr', g), ('blocked', b)):\n"
+        "    r = gbg.bfs(h, 0)\n"
+        "    out[name] = [r.depth.tolist(), r.modes]\n"
+        "print(json.dumps(out))\n" % root)
+    env = dict(os.environ, GBG_BFS_COOP="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    n, pairs = orc.rmat(13, 16 << 13, 1)
+    off, nbr = csr(n, pairs)
+    d, modes, _ = orc.bfs(n, off, nbr, 0)
+    for name in ("csr", "blocked"):
+        assert np.array_equal(np.array(got[name][0], dtype=np.int32), d), name
+        assert got[name][1] == modes, name
