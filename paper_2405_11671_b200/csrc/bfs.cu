@@ -319,15 +319,10 @@ __global__ void first_nbr_k(G g, uint32_t* first, uint32_t* iso) {
 // The persistent path; false when the device cannot co-schedule the grid.
 template <class G>
 bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* st) {
-  int coop = 0;
-  GBG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device));
+  if (!coop_enabled(g->device)) return false;
   int per_sm = 0;
   GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_coop_k<G>, kPushThreads, 0));
-  static const bool disabled = [] {
-    const char* e = std::getenv("GBG_BFS_COOP");
-    return e && e[0] == '0';
-  }();
-  if (!coop || per_sm < 1 || disabled) return false;
+  if (per_sm < 1) return false;
   const unsigned grid = static_cast<unsigned>(per_sm * g->sm_count);
   TraversalBuffers tb(g);
   CoopState s;

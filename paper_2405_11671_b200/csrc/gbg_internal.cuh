@@ -243,6 +243,20 @@ void with_view(gbg_graph* g, F&& f) {
 // current; returns a pointer usable as CSR-like offsets for scheduling.
 const uint64_t* virtual_offsets(gbg_graph* g);
 
+// Persistent cooperative kernels (BFS, k-core, coloring) are used when the
+// device supports cooperative launch, unless GBG_COOP=0 (then the
+// launch-per-step host loops run: the fallback, testable on any device).
+inline bool coop_enabled(int device) {
+  static const bool env_off = [] {
+    const char* e = std::getenv("GBG_COOP");
+    return e && e[0] == '0';
+  }();
+  if (env_off) return false;
+  int coop = 0;
+  cuda_check(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device), "cudaDeviceGetAttribute");
+  return coop != 0;
+}
+
 // Every vertex's first neighbour (traverse.cuh kNoFirst when isolated),
 // kept until the next update (bfs.cu).
 const uint32_t* first_neighbors(gbg_graph* g);

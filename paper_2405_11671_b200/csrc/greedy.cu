@@ -418,8 +418,8 @@ void coloring_run(gbg_graph* g, G view, uint32_t* colors) {
   tr.mark("setup");
   const ColorReleaseOp rel{beats, waiting};
 
-  int coop = 0, per_sm = 0;
-  GBG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device));
+  int per_sm = 0;
+  const int coop = coop_enabled(g->device) ? 1 : 0;
   GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, color_coop_k<G>, kPushThreads, 0));
   uint64_t rounds = 0;
   if (coop && per_sm > 0) {

@@ -216,8 +216,8 @@ void kcore_run(gbg_graph* g, G view, int64_t* core) {
                            g->stream));
   GBG_CUDA(cudaStreamSynchronize(g->stream));  // `init` is pageable and goes out of scope
 
-  int coop = 0, per_sm = 0;
-  GBG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, g->device));
+  int per_sm = 0;
+  const int coop = coop_enabled(g->device) ? 1 : 0;
   GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kcore_coop_k<G>, kPushThreads, 0));
   if (coop && per_sm > 0) {
     KcoreCoop s{deg, core, {alive[0], alive[1]}, {list[0], list[1]}, {dscan[0], dscan[1]}, slot, slot + 3 * kSlot};

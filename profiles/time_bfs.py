@@ -1,5 +1,5 @@
 """BFS at R-MAT s16 / s24 (device-resident depths), CUDA events; per-level
-device times from the library's stats.  GBG_BFS_COOP=0 forces the
+device times from the library's stats.  GBG_COOP=0 forces the
 launch-per-level path."""
 import os
 import sys

@@ -154,10 +154,10 @@ def test_pipelined_create_with_pagerank_layout(gbg, ref, orc):
         gbg.CsrGraph.from_csr(boff, nbr, prepare_pagerank=True)
 
 
-def test_bfs_launch_per_level_path_matches_oracle(gbg, orc, tmp_path):
-    """The launch-per-level BFS (used when cooperative launch is unavailable,
-    forced here with GBG_BFS_COOP=0 in a fresh process) gives the same
-    depths and direction trace as the oracle."""
+def test_launch_per_step_paths_match_oracle(gbg, orc, tmp_path):
+    """The launch-per-step host loops (used when cooperative launch is
+    unavailable; forced here with GBG_COOP=0 in a fresh process) of BFS,
+    k-core and coloring give the oracle's outputs and BFS direction trace."""
     import json
     import os
     import subprocess
@@ -173,15 +173,18 @@ def test_bfs_launch_per_level_path_matches_oracle(gbg, orc, tmp_path):
         "out = {}\n"
         "for name, h in (('csr', g), ('blocked', b)):\n"
         "    r = gbg.bfs(h, 0)\n"
-        "    out[name] = [r.depth.tolist(), r.modes]\n"
+        "    out[name] = [r.depth.tolist(), r.modes, gbg.kcore(h).tolist(), gbg.coloring(h).tolist()]\n"
         "print(json.dumps(out))\n" % root)
-    env = dict(os.environ, GBG_BFS_COOP="0")
-    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, GBG_COOP="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     got = json.loads(res.stdout.strip().splitlines()[-1])
     n, pairs = orc.rmat(13, 16 << 13, 1)
     off, nbr = csr(n, pairs)
     d, modes, _ = orc.bfs(n, off, nbr, 0)
+    core, col = orc.kcore(n, off, nbr), orc.coloring(n, off, nbr)
     for name in ("csr", "blocked"):
         assert np.array_equal(np.array(got[name][0], dtype=np.int32), d), name
         assert got[name][1] == modes, name
+        assert np.array_equal(np.array(got[name][2], dtype=np.uint64), core), name
+        assert np.array_equal(np.array(got[name][3], dtype=np.uint32), col), name
