@@ -176,12 +176,11 @@ def pr_bytes(n: int, m: int, w: int = 8) -> int:
     return w * (n + 1) + 4 * m + 16 * n
 
 
-def bfs_model_bytes(n, off, depth, modes, sizes, degsums, w=8):
-    """SURVEY §8(d) BFS byte model using the modes actually chosen (dense
-    E_scan approximated by the degree of the scanned vertices' prefix is not
-    recomputed here: dense levels count W(n+1) + 3 bm + 4 |N| + 4 E_scan with
-    E_scan <= sum of scanned degrees; we report the lower bound without
-    E_scan)."""
+def bfs_model_bytes(n, modes, sizes, degsums, examined, w=8):
+    """SURVEY §8(d) BFS byte model over the levels actually run: a sparse
+    level moves 4|F| + 2W|F| + 4 sum deg(F) + 8|N| + bm, a dense one
+    W(n+1) + 3 bm + 4 E_scan + 4|N| with E_scan the arcs inspected (the
+    library reports them per level, equal to the reference's)."""
     bm = (n + 7) // 8
     total = 0
     for i, md in enumerate(modes):
@@ -190,7 +189,7 @@ def bfs_model_bytes(n, off, depth, modes, sizes, degsums, w=8):
         if md == 0:
             total += 4 * f + 2 * w * f + 4 * degsums[i] + 8 * nxt + bm
         else:
-            total += w * (n + 1) + 3 * bm + 4 * nxt
+            total += w * (n + 1) + 3 * bm + 4 * examined[i] + 4 * nxt
     return total
 
 
@@ -444,8 +443,10 @@ def main():
                                   "modes": st["modes"], "frontier_sizes": st["frontier_sizes"],
                                   "level_ms": st["level_ms"],
                                   "reached": st["reached"], "source": src,
-                                  "model_bytes_lower_bound": bfs_model_bytes(n, off, d, st["modes"],
-                                                                             st["frontier_sizes"], st["degree_sums"])}
+                                  "examined_arcs": st["examined"]}
+        mb = bfs_model_bytes(n, st["modes"], st["frontier_sizes"], st["degree_sums"], st["examined"])
+        workloads[f"bfs_s{S}"].update({"model_bytes": mb, "model_gbs": mb / tb / 1e9,
+                                       "model_frac_of_hbm": mb / tb / 1e9 / peaks["hbm_gbs"]})
         lab = torch.empty(n, dtype=torch.int32, device="cuda")
         for _ in range(args.warmup):
             gbg.cc_device(g, lab.data_ptr())

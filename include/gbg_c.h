@@ -78,6 +78,10 @@ typedef struct gbg_bfs_stats {
   uint64_t degree_sum[GBG_MAX_LEVELS];   /* sum deg(F) fed to level i      */
   uint64_t reached;                      /* vertices with depth >= 0       */
   float level_ms[GBG_MAX_LEVELS];        /* device time of level i (events) */
+  uint64_t examined[GBG_MAX_LEVELS];     /* arcs inspected by level i in the reference's
+                                            order: sum deg(F) for a push, and for an
+                                            early-exit pull each vertex's list up to
+                                            its first frontier hit (SURVEY §8(d) E_scan) */
 } gbg_bfs_stats;
 
 /* ---- errors / runtime ---------------------------------------------- */

@@ -440,6 +440,15 @@ class Oracle:
             raise ValueError("csr_build: format error")
         return off, nbr[: p.shape[0]]
 
+    def bfs_examined(self, n, off, nbr, src, cap=64):
+        """Arcs inspected per level in the reference's order (sum deg(F) for a
+        push level, list prefixes up to the first hit for a dense one)."""
+        self.L.gbo_bfs_examined.argtypes = [C.c_uint64, _u64p, _u32p, C.c_uint32, _u64p, C.c_uint64]
+        self.L.gbo_bfs_examined.restype = C.c_uint64
+        ex = np.zeros(cap, dtype=np.uint64)
+        k = self.L.gbo_bfs_examined(n, *self._csr_args(off, nbr), src, ptr(ex, _u64p), cap)
+        return [int(x) for x in ex[:min(k, cap)]]
+
     def bfs(self, n, off, nbr, src, cap=64):
         off = np.ascontiguousarray(off, dtype=np.uint64)
         nbr = np.ascontiguousarray(nbr, dtype=np.uint32)

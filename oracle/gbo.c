@@ -742,3 +742,69 @@ uint64_t gbo_bytecode_encode(uint64_t n, const uint64_t* off, const uint32_t* nb
   if (byte_offsets) byte_offsets[n] = pos;
   return pos;
 }
+
+/* Arcs the reference's traversal inspects per BFS level (SURVEY §8(d) E_scan):
+ * a sparse level (edge_map_sparse, traversal.cpp:16-46) maps every
+ * frontier member's whole list, sum deg(F); a dense early-exit level
+ * (edge_map_dense, traversal.cpp:48-95) scans each unvisited vertex's list
+ * in order up to and including its first frontier member.  Same switch rule
+ * and level structure as gbo_bfs.  Returns the number of levels. */
+uint64_t gbo_bfs_examined(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, uint64_t* examined,
+                          uint64_t cap) {
+  if (src >= n) return 0;
+  uint64_t m = off[n];
+  uint64_t nw = (n + 63) / 64;
+  int32_t* depth = (int32_t*)malloc(n * sizeof(int32_t));
+  uint32_t* cur = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+  uint32_t* nxt = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+  uint64_t* fb = (uint64_t*)calloc(nw + 1, sizeof(uint64_t));
+  for (uint64_t v = 0; v < n; ++v) depth[v] = -1;
+  depth[src] = 0;
+  uint64_t fsize = 1, lvl = 0;
+  cur[0] = src;
+  int32_t d = 0;
+  while (fsize > 0) {
+    ++d;
+    uint64_t degsum = 0, ex = 0;
+    for (uint64_t i = 0; i < fsize; ++i) degsum += off[cur[i] + 1] - off[cur[i]];
+    int dense = (double)(fsize + degsum) > (1.0 / 20.0) * (double)m;
+    uint64_t k = 0;
+    if (!dense) {
+      ex = degsum;
+      for (uint64_t i = 0; i < fsize; ++i) {
+        uint32_t u = cur[i];
+        for (uint64_t e = off[u]; e < off[u + 1]; ++e) {
+          uint32_t v = nbr[e];
+          if (depth[v] != -1) continue;
+          depth[v] = d;
+          nxt[k++] = v;
+        }
+      }
+    } else {
+      memset(fb, 0, nw * sizeof(uint64_t));
+      for (uint64_t i = 0; i < fsize; ++i) set_bit(fb, cur[i]);
+      for (uint64_t v = 0; v < n; ++v) {
+        if (depth[v] != -1) continue;
+        for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+          ++ex;
+          if (test_bit(fb, nbr[e])) {
+            nxt[k++] = (uint32_t)v;
+            break;
+          }
+        }
+      }
+      for (uint64_t i = 0; i < k; ++i) depth[nxt[i]] = d;
+    }
+    if (lvl < cap) examined[lvl] = ex;
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+    fsize = k;
+    ++lvl;
+  }
+  free(depth);
+  free(cur);
+  free(nxt);
+  free(fb);
+  return lvl;
+}

@@ -26,6 +26,8 @@ int gbo_bfs(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, 
             int32_t* modes, uint64_t* sizes, uint64_t cap, uint64_t* levels);
 int gbo_pagerank(uint64_t n, const uint64_t* off, const uint32_t* nbr, double damping,
                  uint64_t iters, double tol, double* out);
+uint64_t gbo_bfs_examined(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, uint64_t* examined,
+                          uint64_t cap);
 void gbo_cc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t* labels);
 int gbo_bc(uint64_t n, const uint64_t* off, const uint32_t* nbr, uint32_t src, double* delta);
 uint64_t gbo_tc(uint64_t n, const uint64_t* off, const uint32_t* nbr);

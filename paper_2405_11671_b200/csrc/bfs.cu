@@ -98,6 +98,7 @@ struct CoopState {
   uint32_t src;
   const uint32_t* first;       // first neighbours (dense-level shortcut)
   const uint32_t* iso;         // isolated vertices: pre-set in `visited` (never reached, never pulled)
+  unsigned long long* level_examined;  // [GBG_MAX_LEVELS] arcs inspected by dense levels
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     s.bm[0][w] = 0;
   }
   if (tid < 3) s.packed[tid] = 0;
+  if (tid < GBG_MAX_LEVELS) s.level_examined[tid] = 0;
   grid.sync();
   if (tid == 0) {
     const uint32_t bit = 1u << (s.src & 31);
@@ -183,7 +185,8 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     BfsOp op{s.visited, s.depth, level};
     unsigned long long* acc = s.packed + level % 3;
     if (dense) {
-      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc, s.first);
+      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc, s.first,
+                                 level <= GBG_MAX_LEVELS ? s.level_examined + level - 1 : nullptr);
       has_list = false;
     } else {
       if (!has_list) {
@@ -266,7 +269,8 @@ void ensure_list(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& f) {
 
 // One edge_map step from `cur` into `out` (the other buffer set).
 template <class G, class Op, bool kEarly>
-void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Frontier& out, bool dense, Op op) {
+void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Frontier& out, bool dense, Op op,
+                   unsigned long long* examined = nullptr) {
   GBG_CUDA(cudaMemsetAsync(tb.packed, 0, sizeof(unsigned long long), g->stream));
   out.has_list = out.has_bm = false;
   if (dense) {
@@ -276,7 +280,7 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
       cur.has_bm = true;
     }
     GBG_LAUNCH(g, (pull_k<G, Op, kEarly>), pull_grid(g, tb.nw), kPullThreads, 0, view, cur.bm, op, out.bm, tb.nw,
-               tb.packed, kEarly ? first_neighbors(g) : static_cast<const uint32_t*>(nullptr));
+               tb.packed, kEarly ? first_neighbors(g) : static_cast<const uint32_t*>(nullptr), examined);
     out.has_bm = true;
   } else {
     ensure_list(g, view, tb, cur);
@@ -346,13 +350,17 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.src = src;
   s.first = first_neighbors(g);
   s.iso = isolated_bitmap(g);
+  s.level_examined = g->ws.get<unsigned long long>("bfs.examined", GBG_MAX_LEVELS);
   void* args[] = {&view, &s};
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));
   g->launches++;
   std::vector<uint64_t> hs(3 * GBG_MAX_LEVELS + 8);
   std::vector<int32_t> hm(GBG_MAX_LEVELS);
+  std::vector<unsigned long long> hx(GBG_MAX_LEVELS);
   GBG_CUDA(cudaMemcpyAsync(hs.data(), stat, hs.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
+  GBG_CUDA(cudaMemcpyAsync(hx.data(), s.level_examined, hx.size() * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, g->stream));
   GBG_CUDA(cudaMemcpyAsync(hm.data(), s.level_mode, hm.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
   GBG_CUDA(cudaStreamSynchronize(g->stream));
   if (st) {
@@ -365,6 +373,7 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
       st->frontier[i] = pack_count(hs[i]);
       st->degree_sum[i] = pack_degsum(hs[i]);
       st->level_ms[i] = static_cast<float>((hs[GBG_MAX_LEVELS + i + 1] - hs[GBG_MAX_LEVELS + i]) * 1e-6);
+      st->examined[i] = hm[i] == GBG_MODE_DENSE ? hx[i] : st->degree_sum[i];
     }
   }
   return true;
@@ -387,6 +396,8 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   uint64_t reached = 1;
   int32_t level = 0;
   if (st) std::memset(st, 0, sizeof(*st));
+  unsigned long long* xcnt = g->ws.get<unsigned long long>("bfs.examined", GBG_MAX_LEVELS);
+  GBG_CUDA(cudaMemsetAsync(xcnt, 0, GBG_MAX_LEVELS * sizeof(unsigned long long), g->stream));
   cudaEvent_t ev[GBG_MAX_LEVELS + 1];
   int nev = 0;
   if (st) {
@@ -403,7 +414,8 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
       st->degree_sum[level - 1] = cur->degsum;
     }
     BfsOp op{visited, depth, level};
-    edge_map_step<G, BfsOp, true>(g, view, tb, *cur, *nxt, dense, op);
+    edge_map_step<G, BfsOp, true>(g, view, tb, *cur, *nxt, dense, op,
+                                  st && level <= GBG_MAX_LEVELS ? xcnt + level - 1 : nullptr);
     if (st && nev <= GBG_MAX_LEVELS) {
       GBG_CUDA(cudaEventCreate(&ev[nev]));
       GBG_CUDA(cudaEventRecord(ev[nev], g->stream));
@@ -420,6 +432,11 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   if (st) {
     st->levels = static_cast<uint64_t>(level);
     st->reached = reached;
+    unsigned long long hx[GBG_MAX_LEVELS];
+    GBG_CUDA(cudaMemcpyAsync(hx, xcnt, sizeof(hx), cudaMemcpyDeviceToHost, g->stream));
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+    for (int32_t i = 0; i < level && i < GBG_MAX_LEVELS; ++i)
+      st->examined[i] = st->mode[i] == GBG_MODE_DENSE ? hx[i] : st->degree_sum[i];
   }
 }
 

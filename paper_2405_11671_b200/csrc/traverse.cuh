@@ -274,13 +274,16 @@ __device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { r
 // 82% of the unvisited vertices with edges hit on their first neighbour).
 constexpr uint32_t kNoFirst = 0xffffffffu;
 
+// `examined` (optional): adds the arcs a serial scan in list order would
+// inspect (up to and including the first hit under early exit).
 template <class G, class Op, bool kEarly>
 __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
-                                           unsigned long long* packed, const uint32_t* first = nullptr) {
+                                           unsigned long long* packed, const uint32_t* first = nullptr,
+                                           unsigned long long* examined = nullptr) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  unsigned long long cnt = 0, degsum = 0;
+  unsigned long long cnt = 0, degsum = 0, ex = 0;
   for (uint64_t w = warp0; w < nwords; w += nwarps) {
     const uint64_t v64 = w * 32 + lane;
     const uint32_t v = static_cast<uint32_t>(v64);
@@ -295,12 +298,14 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
         g.seg(v, b, d);
         if (f != kNoFirst && frontier_bit(fb, f) && op.update(f, v)) found = true;
         j0 = 1;
+        ex += d ? 1 : 0;
       } else {
         g.seg(v, b, d);
       }
       const uint32_t lim = found ? 0 : (d < kPullSerial ? d : kPullSerial);
       for (uint32_t j = j0; j < lim; ++j) {
         const uint32_t u = g.at(b + j);
+        ++ex;
         if (frontier_bit(fb, u) && op.update(u, v)) {
           found = true;
           if (kEarly) break;
@@ -327,6 +332,7 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
           if (lane == f) r = op.update(u, vv);
           if (__shfl_sync(0xffffffffu, r, f)) {
             fl = true;
+            if (lane == l) ex += j0 + f + 1 - kPullSerial;
             break;
           }
         } else {
@@ -335,6 +341,7 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
         }
       }
       if (lane == l && fl) found = true;
+      if (lane == l && !(kEarly && fl)) ex += dd - kPullSerial;
     }
     const uint32_t fm = __ballot_sync(0xffffffffu, found);
     if (lane == 0) nb[w] = fm;  // every word written: no clearing pass needed
@@ -346,13 +353,17 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
   }
   degsum = warp_sum(degsum);
   if (lane == 0 && cnt) atomicAdd(packed, (static_cast<unsigned long long>(cnt) << kPackShift) | degsum);
+  if (examined) {
+    ex = warp_sum(ex);
+    if (lane == 0 && ex) atomicAdd(examined, ex);
+  }
 }
 
 template <class G, class Op, bool kEarly>
 __global__ void __launch_bounds__(kPullThreads)
     pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
-           unsigned long long* packed, const uint32_t* __restrict__ first) {
-  pull_words<G, Op, kEarly>(g, fb, op, nb, nwords, packed, first);
+           unsigned long long* packed, const uint32_t* __restrict__ first, unsigned long long* examined) {
+  pull_words<G, Op, kEarly>(g, fb, op, nb, nwords, packed, first, examined);
 }
 
 }  // namespace gbg

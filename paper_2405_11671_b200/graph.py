@@ -106,7 +106,8 @@ _gpp = C.POINTER(C.c_void_p)
 
 class BfsStats(C.Structure):
     _fields_ = [("levels", C.c_uint64), ("mode", C.c_int32 * MAX_LEVELS), ("frontier", C.c_uint64 * MAX_LEVELS),
-                ("degree_sum", C.c_uint64 * MAX_LEVELS), ("reached", C.c_uint64), ("level_ms", C.c_float * MAX_LEVELS)]
+                ("degree_sum", C.c_uint64 * MAX_LEVELS), ("reached", C.c_uint64), ("level_ms", C.c_float * MAX_LEVELS),
+                ("examined", C.c_uint64 * MAX_LEVELS)]
 
 
 class Caps(C.Structure):
@@ -444,13 +445,14 @@ class BfsResult:
     degree_sums: List[int] = field(default_factory=list)
     reached: int = 0
     level_ms: List[float] = field(default_factory=list)
+    examined: List[int] = field(default_factory=list)
 
 
 def _stats(st: BfsStats) -> dict:
     k = min(st.levels, MAX_LEVELS)
     return dict(modes=[st.mode[i] for i in range(k)], frontier_sizes=[st.frontier[i] for i in range(k)],
                 degree_sums=[st.degree_sum[i] for i in range(k)], reached=st.reached,
-                level_ms=[round(st.level_ms[i], 4) for i in range(k)])
+                level_ms=[round(st.level_ms[i], 4) for i in range(k)], examined=[st.examined[i] for i in range(k)])
 
 
 def bfs(g: _Graph, source: int) -> BfsResult:

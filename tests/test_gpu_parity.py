@@ -445,3 +445,26 @@ def test_scale22_update_sequence_matches_golden(gbg):
         assert digest(r.depth) == rec["bfs_digest"] and r.reached == rec["bfs_reached"]
         assert g.delete_batch(fresh) == rec["deleted"]
         assert g.num_edges() == rec["m_after_delete"]
+
+
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
+def test_bfs_examined_arcs(gbg, orc, kind):
+    """gbg_bfs_stats.examined equals the arcs the reference inspects per level
+    (SURVEY App. A3 / oracle gbo_bfs_examined): sum deg(F) for pushes, list
+    prefixes up to the first frontier hit for early-exit pulls."""
+    for S, want in ((16, [9709, 38520, 1569, 1735, 6]), (20, [64840, 624964, 39715, 46114, 139])):
+        g = gbg.generate_rmat(S, 16 << S, 1, RMAT_A, RMAT_B, RMAT_C,
+                              kind=gbg.KIND_CSR if kind == "csr" else gbg.KIND_BLOCKED)
+        assert gbg.bfs(g, 0).examined == want, S
+    n, pairs = orc.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    g = gbg.CsrGraph.build(n, pairs) if kind == "csr" else gbg.BlockedGraph.build(n, pairs)
+    for src in (0, 5, 77):
+        assert gbg.bfs(g, src).examined == orc.bfs_examined(n, off, nbr, src), src
+
+
+def test_scale24_bfs_examined_arcs(gbg):
+    """SURVEY App. A3 at scale 24: 11,810,112 arcs inspected over six levels."""
+    g = gbg.generate_rmat(24, 16 << 24, 1, RMAT_A, RMAT_B, RMAT_C)
+    r = gbg.bfs(g, 0)
+    assert r.examined == [406360, 9510944, 851503, 1038253, 3041, 11]

@@ -509,3 +509,15 @@ def test_greedy_consumers_with_self_loops(ref, orc):
         assert np.array_equal(orc.mis(n, off, nbr, trial), g.mis(trial))
         for a, b in zip(orc.ldd(n, off, nbr, 0.3, trial), g.ldd(0.3, trial)):
             assert np.array_equal(a, b)
+
+
+def test_bfs_examined_arcs_match_survey(orc):
+    """Per-level arcs inspected (measured with the reference
+    library: sorted-order early exit in dense levels)."""
+    n, pairs = orc.rmat(16, 16 << 16, 1)
+    off, nbr = csr(n, pairs)
+    assert orc.bfs_examined(n, off, nbr, 0) == [9709, 38520, 1569, 1735, 6]
+    gd = golden(20)
+    n, pairs = orc.rmat(20, 16 << 20, 1)
+    off, nbr = csr(n, pairs)
+    assert orc.bfs_examined(n, off, nbr, gd["bfs"]["source"]) == [64840, 624964, 39715, 46114, 139]
