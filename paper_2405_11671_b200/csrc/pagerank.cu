@@ -27,7 +27,7 @@
 // unrolled number of edges per thread (all of a thread's id loads, then all
 // of its gathers, in flight at once).  Results are mapped back to original
 // ids at the end.
-#include <cub/device/device_radix_sort.cuh>
+#include "radix.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -95,17 +95,18 @@ struct PrLayout {
 };
 
 // ---------------------------------------------------------------- layout build
+// (degree desc, id asc) as one key: inverted degree above the L id bits
 template <class G>
-__global__ void degree_keys_k(G g, uint64_t* keys) {
+__global__ void degree_keys_k(G g, int L, uint64_t* keys) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < g.n; v += stride)
-    keys[v] = (static_cast<uint64_t>(0xffffffffu - g.degree(static_cast<uint32_t>(v))) << 32) | v;
+    keys[v] = (static_cast<uint64_t>(0xffffffffu - g.degree(static_cast<uint32_t>(v))) << L) | v;
 }
 
-__global__ void order_from_keys_k(const uint64_t* sorted, uint64_t n, uint32_t* ord, uint32_t* pos) {
+__global__ void order_from_keys_k(const uint64_t* sorted, uint64_t n, int L, uint32_t* ord, uint32_t* pos) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
-    const uint32_t v = static_cast<uint32_t>(sorted[r]);
+    const uint32_t v = static_cast<uint32_t>(sorted[r] & ((uint64_t{1} << L) - 1));
     ord[r] = v;
     pos[v] = static_cast<uint32_t>(r);
   }
@@ -113,8 +114,9 @@ __global__ void order_from_keys_k(const uint64_t* sorted, uint64_t n, uint32_t* 
 
 struct SortedDegIn {
   const uint64_t* sorted;
+  int L;
   __device__ __forceinline__ uint64_t operator()(uint64_t r) const {
-    return 0xffffffffu - static_cast<uint32_t>(sorted[r] >> 32);
+    return 0xffffffffu - static_cast<uint32_t>(sorted[r] >> L);
   }
 };
 
@@ -170,19 +172,17 @@ PrLayout* layout_rows(gbg_graph* g, G view) {
   L->n = n;
   L->m = m;
   uint64_t* keys = g->ws.get<uint64_t>("prl.keys", n);
-  uint64_t* sorted = g->ws.get<uint64_t>("prl.sorted", n);
-  GBG_LAUNCH(g, degree_keys_k<G>, grid_for(n, 256), 256, 0, view, keys);
-  size_t temp = 0;
-  GBG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, keys, sorted, n, 0, 64, g->stream));
-  void* tmp = g->ws.get("prl.cub", temp);
-  GBG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, temp, keys, sorted, n, 0, 64, g->stream));
-  g->launches += 9;
+  uint64_t* scratch = g->ws.get<uint64_t>("prl.sorted", n);
+  int idb = 1;  // id bits
+  while ((uint64_t{1} << idb) < n) ++idb;
+  GBG_LAUNCH(g, degree_keys_k<G>, grid_for(n, 256), 256, 0, view, idb, keys);
+  const uint64_t* sorted = radix_sort_u64(g, keys, scratch, n, 32 + idb, "prl.sort");
   L->ord = dalloc<uint32_t>(n);
   L->pos = dalloc<uint32_t>(n);
   L->off = dalloc<uint64_t>(n + 1);
   L->nbr = dalloc<uint32_t>(m);
-  GBG_LAUNCH(g, order_from_keys_k, grid_for(n, 256), 256, 0, sorted, n, L->ord, L->pos);
-  device_scan<uint64_t>(g, SortedDegIn{sorted}, ArrayOut<uint64_t>{L->off}, n, L->off + n, "prl.scan");
+  GBG_LAUNCH(g, order_from_keys_k, grid_for(n, 256), 256, 0, sorted, n, idb, L->ord, L->pos);
+  device_scan<uint64_t>(g, SortedDegIn{sorted, idb}, ArrayOut<uint64_t>{L->off}, n, L->off + n, "prl.scan");
   uint32_t* bnd = g->ws.get<uint32_t>("prl.bnd", kClasses);
   GBG_LAUNCH(g, class_bounds_k, 1, 32, 0, L->off, n, bnd);
   uint32_t hb[kClasses];
@@ -213,7 +213,8 @@ PrLayout* layout_rows(gbg_graph* g, G view) {
   GBG_CUDA(cudaMemsetAsync(L->done_counter, 0, sizeof(unsigned), g->stream));
   g->ws.release("prl.keys");
   g->ws.release("prl.sorted");
-  g->ws.release("prl.cub");
+  g->ws.release("prl.sort.hist");
+  g->ws.release("prl.sort.lb");
   return L.release();
 }
 

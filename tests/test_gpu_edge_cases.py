@@ -188,3 +188,35 @@ def test_launch_per_step_paths_match_oracle(gbg, orc, tmp_path):
         assert got[name][1] == modes, name
         assert np.array_equal(np.array(got[name][2], dtype=np.uint64), core), name
         assert np.array_equal(np.array(got[name][3], dtype=np.uint32), col), name
+
+
+def test_concurrent_reads_from_threads(gbg, orc):
+    """graph_container.hpp:33-35: read operations are safe from many threads.
+    Several host threads run BFS / CC / degree queries on one handle (calls
+    are serialised per handle) and on their own handles at once."""
+    import threading
+
+    n, pairs = orc.rmat(12, 16 << 12, 1)
+    off, nbr = csr(n, pairs)
+    want_d = orc.bfs(n, off, nbr, 0)[0]
+    want_cc = orc.cc(n, off, nbr)
+    shared = gbg.CsrGraph.build(n, pairs)
+    errors = []
+
+    def worker(k):
+        try:
+            own = gbg.BlockedGraph.build(n, pairs)
+            for _ in range(5):
+                for g in (shared, own):
+                    assert np.array_equal(gbg.bfs(g, 0).depth, want_d)
+                    assert np.array_equal(gbg.cc(g), want_cc)
+                    assert g.degree(k) == int(off[k + 1] - off[k])
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:3]
