@@ -167,6 +167,14 @@ gbg_status gbg_memory_bytes(const gbg_graph* g, uint64_t* bytes);
 gbg_status gbg_subset_to_dense(uint64_t n, const uint32_t* ids, uint64_t k, uint64_t* words);
 /* to_sparse (vertex_subset.cpp:39-45): words -> ascending ids; *k = size. */
 gbg_status gbg_subset_to_sparse(uint64_t n, const uint64_t* words, uint32_t* ids, uint64_t* k);
+/* vertex_filter (traversal.cpp:117-131) with pred(v) = keep[v] != 0, in the
+ * input's representation: sparse ids[k] -> out[*out_k] (ascending and
+ * unique, as VertexSubset's constructor makes them, vertex_subset.cpp:8-15;
+ * out holds k entries), dense words -> out_words.  vertex_map (traversal.cpp:113-115) applies a
+ * host callback per member and has nothing to offload. */
+gbg_status gbg_vertex_filter_sparse(uint64_t n, const uint32_t* ids, uint64_t k, const uint8_t* keep,
+                                    uint32_t* out, uint64_t* out_k);
+gbg_status gbg_vertex_filter_dense(uint64_t n, const uint64_t* words, const uint8_t* keep, uint64_t* out_words);
 
 /* ---- edge_map (traversal.hpp:37-56 / traversal.cpp:16-111) ---------- */
 /* One edge_map over frontier ids[k] with cond(v) = cond_mask[v] != 0 and an

@@ -151,6 +151,22 @@ class Ref:
     def hash_combine(self, a: int, b: int) -> int:
         return self.L.gbref_hash_combine(a, b)
 
+    def vertex_filter_sparse(self, n, ids, keep):
+        """vertex_filter (traversal.cpp:117-131) on a sparse VertexSubset."""
+        self._bind_vertex_filter()
+        return _ref_vertex_filter(self, n, ids, None, keep)
+
+    def vertex_filter_dense(self, n, words, keep):
+        """vertex_filter on a dense VertexSubset; the result stays dense."""
+        self._bind_vertex_filter()
+        return _ref_vertex_filter(self, n, None, words, keep)
+
+    def _bind_vertex_filter(self):
+        f = self.L.gbref_vertex_filter
+        f.argtypes = [C.c_uint64, _u32p, C.c_uint64, _u64p, _u8p, _u32p, _u64p, C.POINTER(C.c_uint64),
+                      C.POINTER(C.c_int)]
+        f.restype = C.c_int
+
     def log1p(self, x):
         """std::log1p as the reference's C library computes it (rng.hpp:33)."""
         self.L.gbref_log1p.argtypes = [_f64p, C.c_uint64, _f64p]
@@ -337,6 +353,28 @@ class RefCsr:
                                                   int(early_exit), ptr(out, _u8p), C.byref(upd),
                                                   C.byref(chosen)))
         return out.astype(bool), upd.value, chosen.value
+
+
+def _ref_vertex_filter(ref, n, ids, words, keep):
+    keep = np.ascontiguousarray(keep, dtype=np.uint8)
+    k = C.c_uint64(0)
+    dense = C.c_int(0)
+    nw = (n + 63) // 64
+    out_words = np.zeros(max(nw, 1), dtype=np.uint64)
+    if words is None:
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        out_ids = np.empty(max(ids.size, 1), dtype=np.uint32)
+        ref._check(ref.L.gbref_vertex_filter(n, ptr(ids, _u32p), ids.size, None, ptr(keep, _u8p),
+                                             ptr(out_ids, _u32p), ptr(out_words, _u64p), C.byref(k),
+                                             C.byref(dense)))
+        assert not dense.value
+        return out_ids[: k.value].copy()
+    words = np.ascontiguousarray(words, dtype=np.uint64)
+    out_ids = np.empty(1, dtype=np.uint32)
+    ref._check(ref.L.gbref_vertex_filter(n, None, 0, ptr(words, _u64p), ptr(keep, _u8p), ptr(out_ids, _u32p),
+                                         ptr(out_words, _u64p), C.byref(k), C.byref(dense)))
+    assert dense.value
+    return out_words[:nw].copy()
 
 
 class RefChunked:

@@ -368,6 +368,27 @@ int gbref_edge_map(void* csr, const uint32_t* ids, uint64_t nids,
   });
 }
 
+// vertex_filter (traversal.cpp:117-131), pred(v) = keep[v] != 0.  words ==
+// nullptr: sparse input ids[k] -> out_ids[*out_k] in the reference's order;
+// else dense input -> out_words (and *out_k = member count).  *out_dense
+// reports the output representation.
+int gbref_vertex_filter(uint64_t n, const uint32_t* ids, uint64_t k, const uint64_t* words,
+                        const uint8_t* keep, uint32_t* out_ids, uint64_t* out_words,
+                        uint64_t* out_k, int* out_dense) {
+  return guard([&] {
+    VertexSubset s = words ? VertexSubset(n, std::vector<uint64_t>(words, words + (n + 63) / 64),
+                                          VertexSubset::Repr::Dense)
+                           : VertexSubset(n, std::vector<VertexId>(ids, ids + k));
+    VertexSubset r = vertex_filter(s, [&](VertexId v) { return keep[v] != 0; });
+    *out_dense = r.is_dense() ? 1 : 0;
+    *out_k = r.size();
+    if (r.is_dense())
+      std::copy(r.words().begin(), r.words().end(), out_words);
+    else
+      std::copy(r.ids().begin(), r.ids().end(), out_ids);
+  });
+}
+
 // ---- batches ----
 int gbref_update_batch(uint64_t log2_n, double a, double b, double c,
                        uint64_t size, uint64_t seed, uint32_t* out_pairs) {

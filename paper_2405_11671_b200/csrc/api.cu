@@ -59,6 +59,30 @@ __global__ void list_to_bitmap_k(const uint32_t* ids, uint64_t k, uint32_t* bm) 
   }
 }
 
+// vertex_filter (traversal.cpp:117-131): members with keep[v] != 0, in the
+// input's representation (sparse: order kept; dense: word-wise AND)
+struct KeepIn {
+  const uint32_t* ids;
+  const uint8_t* keep;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return keep[ids[i]] != 0; }
+};
+struct KeepOut {
+  const uint32_t* ids;
+  const uint8_t* keep;
+  uint32_t* out;
+  __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
+    if (keep[ids[i]]) out[pre] = ids[i];
+  }
+};
+__global__ void filter_dense_k(uint64_t n, const uint32_t* in, const uint8_t* keep, uint32_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~uint64_t{31}; base < n; base += stride) {
+    const uint64_t v = base + (threadIdx.x & 31);
+    const uint32_t m = __ballot_sync(0xffffffffu, v < n && keep[v] != 0);
+    if ((threadIdx.x & 31) == 0) out[base >> 5] = in[base >> 5] & m;
+  }
+}
+
 // csr.cpp:14-18 split in two passes: the offsets are monotone from 0 to m
 // (vertex-parallel), then every id is in range and strictly above its
 // predecessor within the segment (edge-parallel, balanced).
@@ -529,6 +553,64 @@ gbg_status gbg_subset_to_dense(uint64_t n, const uint32_t* ids, uint64_t k, uint
     (void)nw32;
     if (nw64)
       GBG_CUDA(cudaMemcpyAsync(words, bm, nw64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+  });
+}
+
+gbg_status gbg_vertex_filter_sparse(uint64_t n, const uint32_t* ids, uint64_t k, const uint8_t* keep, uint32_t* out,
+                                    uint64_t* out_k) {
+  return guard([&] {
+    if (!out_k || (k && (!ids || !out)) || (n && !keep)) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    if (k > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "subset too large");
+    bool canonical = true;  // strictly increasing, as VertexSubset stores ids
+    for (uint64_t i = 0; i < k; ++i) {
+      if (ids[i] >= n) fail(GBG_ERR_OUT_OF_RANGE, "VertexSubset: id out of range");
+      if (i && ids[i] <= ids[i - 1]) canonical = false;
+    }
+    *out_k = 0;
+    if (!k) return;
+    std::unique_ptr<gbg_graph> g(new_handle(GBG_KIND_CSR, n));
+    AllocStream as(g->stream);
+    uint32_t* dids = g->ws.get<uint32_t>("ids", k);
+    uint32_t* dout = g->ws.get<uint32_t>("out", k);
+    uint8_t* dkeep = g->ws.get<uint8_t>("keep", n);
+    uint32_t* cnt = g->ws.get<uint32_t>("cnt", 1);
+    GBG_CUDA(cudaMemcpyAsync(dids, ids, k * sizeof(uint32_t), cudaMemcpyHostToDevice, g->stream));
+    GBG_CUDA(cudaMemcpyAsync(dkeep, keep, n, cudaMemcpyHostToDevice, g->stream));
+    if (canonical) {  // order-preserving compaction, O(k)
+      device_scan<uint32_t>(g.get(), KeepIn{dids, dkeep}, KeepOut{dids, dkeep, dout}, k, cnt, "vf");
+    } else {  // the constructor's sort + unique (vertex_subset.cpp:8-15) through a bitmap
+      const uint64_t nw64 = (n + 63) / 64;
+      uint32_t* bm = g->ws.get<uint32_t>("bm", 2 * nw64);
+      uint32_t* fm = g->ws.get<uint32_t>("fm", 2 * nw64);
+      GBG_CUDA(cudaMemsetAsync(bm, 0, 2 * nw64 * sizeof(uint32_t), g->stream));
+      GBG_LAUNCH(g.get(), list_to_bitmap_k, grid_for(k, 256), 256, 0, dids, k, bm);
+      GBG_LAUNCH(g.get(), filter_dense_k, grid_for((n + 31) / 32 * 32, 256), 256, 0, n, bm, dkeep, fm);
+      bitmap_to_list(g.get(), fm, (n + 31) / 32, dout, cnt);
+    }
+    uint32_t hc = 0;
+    read_scalars(g.get(), cnt, sizeof(hc), &hc);
+    if (hc) GBG_CUDA(cudaMemcpyAsync(out, dout, hc * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+    GBG_CUDA(cudaStreamSynchronize(g->stream));
+    *out_k = hc;
+  });
+}
+
+gbg_status gbg_vertex_filter_dense(uint64_t n, const uint64_t* words, const uint8_t* keep, uint64_t* out_words) {
+  return guard([&] {
+    if (n && (!words || !keep || !out_words)) fail(GBG_ERR_INVALID_ARGUMENT, "null argument");
+    const uint64_t nw64 = (n + 63) / 64;
+    if (!nw64) return;
+    std::unique_ptr<gbg_graph> g(new_handle(GBG_KIND_CSR, n));
+    AllocStream as(g->stream);
+    uint32_t* din = g->ws.get<uint32_t>("in", 2 * nw64);
+    uint32_t* dout = g->ws.get<uint32_t>("out", 2 * nw64);
+    uint8_t* dkeep = g->ws.get<uint8_t>("keep", n);
+    GBG_CUDA(cudaMemcpyAsync(din, words, nw64 * sizeof(uint64_t), cudaMemcpyHostToDevice, g->stream));
+    GBG_CUDA(cudaMemcpyAsync(dkeep, keep, n, cudaMemcpyHostToDevice, g->stream));
+    GBG_CUDA(cudaMemsetAsync(dout, 0, 2 * nw64 * sizeof(uint32_t), g->stream));
+    GBG_LAUNCH(g.get(), filter_dense_k, grid_for((n + 31) / 32 * 32, 256), 256, 0, n, din, dkeep, dout);
+    GBG_CUDA(cudaMemcpyAsync(out_words, dout, nw64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
     GBG_CUDA(cudaStreamSynchronize(g->stream));
   });
 }

@@ -137,6 +137,8 @@ _SIGS = {
     "gbg_memory_bytes": [_vp, _u64p],
     "gbg_subset_to_dense": [C.c_uint64, _u32p, C.c_uint64, _u64p],
     "gbg_subset_to_sparse": [C.c_uint64, _u64p, _u32p, _u64p],
+    "gbg_vertex_filter_sparse": [C.c_uint64, _u32p, C.c_uint64, _u8p, _u32p, _u64p],
+    "gbg_vertex_filter_dense": [C.c_uint64, _u64p, _u8p, _u64p],
     "gbg_edge_map": [_vp, _u32p, C.c_uint64, _u8p, C.c_int, C.c_int, _u8p, _u64p, C.POINTER(C.c_int)],
     "gbg_bfs": [_vp, C.c_uint32, _i32p, C.POINTER(BfsStats)],
     "gbg_bfs_device": [_vp, C.c_uint32, _vp, C.POINTER(BfsStats)],
@@ -564,6 +566,26 @@ def triangle_count(g: _Graph) -> int:
     t = C.c_uint64()
     _check(_L.gbg_tc(g.handle, C.byref(t)))
     return t.value
+
+
+def vertex_filter_sparse(n: int, ids, keep) -> np.ndarray:
+    """vertex_filter (traversal.cpp:117-131) on a sparse subset: the members
+    with keep[v] != 0, ascending and unique as VertexSubset holds them."""
+    a = np.ascontiguousarray(ids, dtype=np.uint32)
+    k = np.ascontiguousarray(keep, dtype=np.uint8)
+    out = np.empty(max(a.size, 1), dtype=np.uint32)
+    cnt = C.c_uint64()
+    _check(_L.gbg_vertex_filter_sparse(n, _p(a, _u32p), a.size, _p(k, _u8p), _p(out, _u32p), C.byref(cnt)))
+    return out[: cnt.value]
+
+
+def vertex_filter_dense(n: int, words, keep) -> np.ndarray:
+    """vertex_filter on a dense subset (uint64 words, LSB first): stays dense."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    k = np.ascontiguousarray(keep, dtype=np.uint8)
+    out = np.zeros(max(w.size, 1), dtype=np.uint64)
+    _check(_L.gbg_vertex_filter_dense(n, _p(w, _u64p), _p(k, _u8p), _p(out, _u64p)))
+    return out[: w.size]
 
 
 def edge_map(g: _Graph, frontier_ids, cond_mask, mode: int = MODE_AUTO, early_exit: bool = True):

@@ -43,6 +43,33 @@ def test_subset_round_trips(gbg, orc):
         assert np.array_equal(gbg.subset_to_sparse(n, dense), orc.to_sparse(n, dense))
 
 
+def test_vertex_filter_reference_cases(gbg):
+    # test_traversal.cpp:239-261
+    evens = [1, 0, 1, 0, 1, 0]
+    assert gbg.vertex_filter_sparse(6, [0, 1, 2, 3], evens).tolist() == [0, 2]
+    assert gbg.vertex_filter_sparse(6, [0, 1, 2, 3], [1] * 6).tolist() == [0, 1, 2, 3]
+    dense = gbg.subset_to_dense(6, [0, 1, 2, 3])
+    out = gbg.vertex_filter_dense(6, dense, [1, 1, 0, 0, 0, 0])
+    assert gbg.subset_to_sparse(6, out).tolist() == [0, 1]
+    assert gbg.vertex_filter_sparse(6, [], evens).size == 0
+    assert gbg.vertex_filter_sparse(6, [5, 2, 2, 0], evens).tolist() == [0, 2]  # constructor sorts + dedups
+    with pytest.raises(IndexError):
+        gbg.vertex_filter_sparse(4, [4], [1] * 4)
+
+
+def test_vertex_filter_matches_reference(gbg, ref):
+    rng = np.random.default_rng(7)
+    for trial in range(120):
+        n = int(rng.integers(1, 70000 if trial % 10 == 0 else 3000))
+        keep = (rng.random(n) < rng.random()).astype(np.uint8)
+        ids = rng.integers(0, n, size=int(rng.integers(0, n + 1))).astype(np.uint32)
+        if trial % 2:
+            ids = np.unique(ids)
+        assert np.array_equal(gbg.vertex_filter_sparse(n, ids, keep), ref.vertex_filter_sparse(n, ids, keep))
+        words = gbg.subset_to_dense(n, ids)
+        assert np.array_equal(gbg.vertex_filter_dense(n, words, keep), ref.vertex_filter_dense(n, words, keep))
+
+
 # ---------------------------------------------------------------- containers
 def test_csr_build_and_read_api(gbg):
     g = gbg.CsrGraph.build(4, T4_PAIRS)

@@ -98,6 +98,16 @@ def test_subset_round_trips(orc):
 
 
 # ---------------------------------------------------------------- edge_map
+def test_ref_vertex_filter_known_answers(ref):
+    # test_traversal.cpp:239-261 through the compiled reference
+    evens = [1, 0, 1, 0, 1, 0]
+    assert ref.vertex_filter_sparse(6, [0, 1, 2, 3], evens).tolist() == [0, 2]
+    assert ref.vertex_filter_sparse(6, [0, 1, 2, 3], [1] * 6).tolist() == [0, 1, 2, 3]
+    out = ref.vertex_filter_dense(6, np.array([0b1111], np.uint64), [1, 1, 0, 0, 0, 0])
+    assert out.tolist() == [0b11]
+    assert ref.vertex_filter_sparse(6, [5, 2, 2, 0], evens).tolist() == [0, 2]
+
+
 def test_edge_map_known_answers(ref, orc):
     off, nbr = csr(4, T4_PAIRS)
     g = ref.csr(4, off, nbr)
