@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "libgbg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--extended-lambda", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "-Xptxas", "-O3", "-DNDEBUG"]
+         "-Xptxas", "-O3", "-DNDEBUG"] + os.environ.get("GBG_NVCC_EXTRA", "").split()
 
 
 def _headers():

@@ -24,7 +24,7 @@ namespace gbg {
 // BFS as an edge_map operator: cond = unvisited, claim = atomic test-and-set
 // on the visited bitmap (AtomicBitset::try_claim, parallel.hpp:133-137),
 // update = record the depth.  In pull mode the warp owning a 32-vertex word
-// publishes visited bits without atomics (dense_word).
+// publishes its word's visited bits with one reduction (dense_word).
 struct BfsOp {
   uint32_t* visited;
   int32_t* depth;
@@ -40,7 +40,9 @@ struct BfsOp {
     depth[v] = level;
     return true;
   }
-  __device__ __forceinline__ void dense_word(uint64_t w, uint32_t m) const { visited[w] |= m; }
+  // the owning warp's word: a fire-and-forget reduction (RED.OR) instead of
+  // a load + store keeps one L2 round trip off every word's chain
+  __device__ __forceinline__ void dense_word(uint64_t w, uint32_t m) const { atomicOr(visited + w, m); }
 };
 
 // The test operator of gbg_edge_map: cond from a byte mask, a fresh claim
