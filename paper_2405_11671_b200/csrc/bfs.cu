@@ -88,7 +88,7 @@ struct CoopState {
   int32_t* depth;
   uint32_t* list[2];
   uint64_t* dscan[2];
-  uint32_t* bm[2];
+  uint32_t* bm[3];             // frontier bitmaps: level l reads bm[(l-1)%3], writes bm[l%3], clears bm[(l+1)%3]
   unsigned long long* packed;  // ring of 3 level counters
   uint64_t* level_packed;      // [GBG_MAX_LEVELS] per-level (count, degsum) of the input frontier
   int32_t* level_mode;         // [GBG_MAX_LEVELS]
@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
   for (uint64_t w = tid; w < s.nw; w += nthreads) {
     s.visited[w] = s.iso[w];
     s.bm[0][w] = 0;
+    s.bm[1][w] = 0;
   }
   if (tid < 3) s.packed[tid] = 0;
   if (tid < GBG_MAX_LEVELS) s.level_examined[tid] = 0;
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     s.level_ns[0] = globaltimer();
   }
   grid.sync();
-  int cur = 0;
+  int cur = 0;      // list buffers
+  int bcur = 0;     // bitmap ring position of the level's input
   bool has_list = true;
   uint64_t reached = 1;
   int32_t level = 1;
@@ -184,31 +186,35 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
       }
     }
     const int nxt = cur ^ 1;
+    const int bnxt = bcur == 2 ? 0 : bcur + 1, bclr = bnxt == 2 ? 0 : bnxt + 1;
     BfsOp op{s.visited, s.depth, level};
     unsigned long long* acc = s.packed + level % 3;
+    // the next level's output bitmap, idle during this level (it was the
+    // previous level's input): cleared here so a sparse level needs no
+    // barrier between clearing and pushing
+    for (uint64_t w = tid; w < s.nw; w += nthreads) s.bm[bclr][w] = 0;
     if (dense) {
-      pull_words<G, BfsOp, true>(g, s.bm[cur], op, s.bm[nxt], s.nw, acc, s.first,
+      pull_words<G, BfsOp, true>(g, s.bm[bcur], op, s.bm[bnxt], s.nw, acc, s.first,
                                  level <= GBG_MAX_LEVELS ? s.level_examined + level - 1 : nullptr);
       has_list = false;
     } else {
       if (!has_list) {
-        coop_bitmap_to_list(grid, g, s.bm[cur], s.nw, s.list[cur], s.dscan[cur], s.blocksum, s_red);
+        coop_bitmap_to_list(grid, g, s.bm[bcur], s.nw, s.list[cur], s.dscan[cur], s.blocksum, s_red);
         has_list = true;
+        grid.sync();
       }
-      if (tid == 0) s.dscan[cur][size] = degsum;  // sentinel closing the last segment
-      for (uint64_t w = tid; w < s.nw; w += nthreads) s.bm[nxt][w] = 0;
-      grid.sync();
       const uint32_t ipt = push_ipt(degsum, gridDim.x);
       const uint64_t tiles = push_tiles(degsum, ipt);
       for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         push_tile(g, s.list[cur], static_cast<uint32_t>(size), s.dscan[cur], degsum, op, s.list[nxt], s.dscan[nxt],
-                  s.bm[nxt], acc, t, s_idx, ipt);
+                  s.bm[bnxt], acc, t, s_idx, ipt);
         __syncthreads();
       }
     }
     grid.sync();
     if (tid == 0 && level <= GBG_MAX_LEVELS) s.level_ns[level] = globaltimer();
     cur = nxt;
+    bcur = bnxt;
   }
   if (tid == 0) {
     s.result[0] = static_cast<uint64_t>(level - 1);
@@ -340,6 +346,7 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.dscan[1] = tb.b.dscan;
   s.bm[0] = tb.a.bm;
   s.bm[1] = tb.b.bm;
+  s.bm[2] = g->ws.get<uint32_t>("bfs.bm2", tb.nw + 2);
   s.packed = g->ws.get<unsigned long long>("bfs.ring", 4);
   uint64_t* stat = g->ws.get<uint64_t>("bfs.stat", 3 * GBG_MAX_LEVELS + 8);
   s.level_packed = stat;
