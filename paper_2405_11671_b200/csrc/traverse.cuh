@@ -145,11 +145,40 @@ __device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, c
   const uint64_t e0 = tile * tile_len;
   if (e0 >= E) return;
   const uint32_t len = static_cast<uint32_t>(E - e0 < tile_len ? E - e0 : tile_len);
+  // The tile's slot range [tlo, thi) first, by a CTA-wide 128-ary search
+  // (each half of the CTA narrows one end per barrier): a per-thread binary
+  // search over a large frontier is ~20 dependent loads, this is ~3 rounds,
+  // and the per-thread searches below then stay inside the tile's slice.
+  uint32_t tlo = 0, thi = nf;
+  if (nf > 64) {
+    const uint32_t half = threadIdx.x >> 7, t = threadIdx.x & 127;
+    const uint64_t key = half ? e0 + len - 1 : e0;
+    uint32_t lo = 0, hi = nf;  // dscan[lo] <= key < dscan[hi] (dscan[nf] := E)
+    while (true) {
+      const bool more = hi - lo > 32;
+      const uint32_t step = (hi - lo + 127) / 128;
+      const uint32_t p = lo + t * step;
+      const bool le = more && p < hi && dscan[p] <= key;
+      const uint32_t c_lo = __syncthreads_count(le && !half);
+      const uint32_t c_hi = __syncthreads_count(le && half);
+      const uint32_t c = half ? c_hi : c_lo;
+      if (!__syncthreads_or(more)) break;
+      if (more) {
+        lo = lo + (c - 1) * step;
+        hi = lo + step < hi ? lo + step : hi;
+      }
+    }
+    if (t == 0) s_idx[half] = half ? hi : lo;
+    __syncthreads();
+    tlo = s_idx[0];
+    thi = s_idx[1];
+    __syncthreads();
+  }
   {
     const uint32_t k0 = threadIdx.x * ipt;
     if (k0 < len) {
       const uint64_t e = e0 + k0;
-      uint32_t lo = 0, hi = nf;  // dscan[lo] <= e < dscan[hi]
+      uint32_t lo = tlo, hi = thi;  // dscan[lo] <= e < dscan[hi]
       while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
         if (dscan[mid] <= e) lo = mid; else hi = mid;
