@@ -32,6 +32,7 @@ struct BfsOp {
   __device__ __forceinline__ bool cond(uint32_t v) const {
     return !((*(volatile uint32_t*)(visited + (v >> 5)) >> (v & 31)) & 1u);
   }
+  __device__ __forceinline__ uint32_t cond_word(uint64_t w) const { return ~*(volatile uint32_t*)(visited + w); }
   __device__ __forceinline__ bool claim(uint32_t v) const {
     const uint32_t bit = 1u << (v & 31);
     return !(atomicOr(visited + (v >> 5), bit) & bit);

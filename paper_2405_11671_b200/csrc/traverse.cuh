@@ -20,6 +20,9 @@
 // (vertex_subset.hpp:10-14).
 #pragma once
 
+#include <type_traits>
+#include <utility>
+
 #include "scan.cuh"
 
 namespace gbg {
@@ -303,12 +306,119 @@ __device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { r
 // 82% of the unvisited vertices with edges hit on their first neighbour).
 constexpr uint32_t kNoFirst = 0xffffffffu;
 
+// Early-exit pull for operators whose cond is a bitmap (Op::cond_word(w):
+// the 32 cond bits of word w).  Each warp owns a contiguous run of words and
+// reads their cond words 32 at a time in one coalesced load, so a word's
+// dependent chain starts at first[] / the row bounds instead of at its cond
+// word, and words without a live vertex cost nothing.
+template <class G, class Op>
+__device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
+                                              unsigned long long* packed, const uint32_t* first,
+                                              unsigned long long* examined) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t per = (nwords + nwarps - 1) / nwarps;
+  const uint64_t wbeg = gwarp * per;
+  const uint64_t wend = wbeg + per < nwords ? wbeg + per : nwords;
+  unsigned long long cnt = 0, degsum = 0, ex = 0;
+  for (uint64_t wb = wbeg; wb < wend; wb += 32) {
+    const uint64_t wl = wb + lane;
+    uint32_t cw = 0;
+    if (wl < wend) {
+      cw = op.cond_word(wl);
+      if (wl * 32 + 32 > g.n) cw &= g.n > wl * 32 ? (1u << (g.n - wl * 32)) - 1u : 0u;
+    }
+    if (wl < wend && !cw) nb[wl] = 0;
+    uint32_t live = __ballot_sync(0xffffffffu, cw != 0);
+    while (live) {
+      const int j = __ffs(live) - 1;
+      live &= live - 1;
+      const uint64_t w = wb + j;
+      const uint32_t v = static_cast<uint32_t>(w * 32 + lane);
+      const bool c = (__shfl_sync(0xffffffffu, cw, j) >> lane) & 1u;
+      uint64_t b = 0;
+      uint32_t d = 0;
+      bool found = false;
+      uint32_t lim = 0;
+      if (c) {
+        const uint32_t f = __ldg(first + v);
+        g.seg(v, b, d);
+        if (f != kNoFirst && frontier_bit(fb, f) && op.update(f, v)) found = true;
+        ex += d ? 1 : 0;
+        lim = found ? 0 : (d < kPullSerial ? d : kPullSerial);
+      }
+      for (uint32_t k = 1; k < lim; ++k) {
+        const uint32_t u = g.at(b + k);
+        ++ex;
+        if (frontier_bit(fb, u) && op.update(u, v)) {
+          found = true;
+          break;
+        }
+      }
+      uint32_t hard = __ballot_sync(0xffffffffu, c && d > kPullSerial && !found);
+      while (hard) {
+        const int l = __ffs(hard) - 1;
+        hard &= hard - 1;
+        const uint64_t bb = __shfl_sync(0xffffffffu, b, l);
+        const uint32_t dd = __shfl_sync(0xffffffffu, d, l);
+        const uint32_t vv = static_cast<uint32_t>(w * 32 + l);
+        bool fl = false;
+        for (uint32_t j0 = kPullSerial; j0 < dd; j0 += 32) {
+          const uint32_t jj = j0 + lane;
+          uint32_t u = 0;
+          const bool hit = jj < dd && frontier_bit(fb, u = g.at(bb + jj));
+          const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+          if (!hm) continue;
+          const int fi = __ffs(hm) - 1;
+          bool r = false;
+          if (lane == fi) r = op.update(u, vv);
+          if (__shfl_sync(0xffffffffu, r, fi)) {
+            fl = true;
+            if (lane == l) ex += j0 + fi + 1 - kPullSerial;
+            break;
+          }
+        }
+        if (lane == l) {
+          if (fl) found = true;
+          else ex += dd - kPullSerial;
+        }
+      }
+      const uint32_t fm = __ballot_sync(0xffffffffu, found);
+      if (lane == 0) {
+        nb[w] = fm;
+        if (fm) op.dense_word(w, fm);
+      }
+      cnt += __popc(fm) * (lane == 0);
+      if (found) degsum += d;
+    }
+  }
+  cnt = warp_sum(cnt);
+  degsum = warp_sum(degsum);
+  if (lane == 0 && cnt) atomicAdd(packed, (static_cast<unsigned long long>(cnt) << kPackShift) | degsum);
+  if (examined) {
+    ex = warp_sum(ex);
+    if (lane == 0 && ex) atomicAdd(examined, ex);
+  }
+}
+
+template <class Op, class = void>
+struct HasCondWord : std::false_type {};
+template <class Op>
+struct HasCondWord<Op, decltype(void(std::declval<const Op&>().cond_word(uint64_t{0})))> : std::true_type {};
+
 // `examined` (optional): adds the arcs a serial scan in list order would
 // inspect (up to and including the first hit under early exit).
 template <class G, class Op, bool kEarly>
 __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
                                            unsigned long long* packed, const uint32_t* first = nullptr,
                                            unsigned long long* examined = nullptr) {
+  if constexpr (kEarly && HasCondWord<Op>::value) {
+    if (first) {
+      pull_words_cw(g, fb, op, nb, nwords, packed, first, examined);
+      return;
+    }
+  }
   const int lane = threadIdx.x & 31;
   const uint64_t warp0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
