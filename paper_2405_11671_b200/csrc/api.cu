@@ -22,7 +22,7 @@ thread_local int t_device = -1;
 void set_last_error(const std::string& m) { t_err = m; }
 
 void read_scalars(gbg_graph* g, const void* dev, size_t bytes, void* host) {
-  if (bytes > 64) fail(GBG_ERR_LOGIC, "read_scalars: too large");
+  if (bytes > kHostScalarBytes) fail(GBG_ERR_LOGIC, "read_scalars: too large");
   GBG_CUDA(cudaMemcpyAsync(g->hscalar, dev, bytes, cudaMemcpyDeviceToHost, g->stream));
   GBG_CUDA(cudaStreamSynchronize(g->stream));
   std::memcpy(host, g->hscalar, bytes);
@@ -41,7 +41,7 @@ gbg_graph* new_handle(int kind, uint64_t n) {
     GBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, g->device));
     uint64_t keep = UINT64_MAX;  // keep freed blocks in the pool for reuse
     GBG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    GBG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g->hscalar), 64));
+    GBG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g->hscalar), kHostScalarBytes));
   } catch (...) {
     delete g;
     throw;

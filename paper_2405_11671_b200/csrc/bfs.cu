@@ -147,24 +147,20 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
   __shared__ uint64_t s_red[33];
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = tid; i < g.n; i += nthreads) s.depth[i] = -1;
+  // initial state, the source included, in one pass and one barrier
+  const uint64_t sw = s.src >> 5;
+  const uint32_t sbit = 1u << (s.src & 31);
+  for (uint64_t i = tid; i < g.n; i += nthreads) s.depth[i] = i == s.src ? 0 : -1;
   for (uint64_t w = tid; w < s.nw; w += nthreads) {
-    s.visited[w] = s.iso[w];
-    s.bm[0][w] = 0;
+    s.visited[w] = s.iso[w] | (w == sw ? sbit : 0u);
+    s.bm[0][w] = w == sw ? sbit : 0u;
     s.bm[1][w] = 0;
   }
-  if (tid < 3) s.packed[tid] = 0;
+  if (tid < 3) s.packed[tid] = tid == 0 ? (1ull << kPackShift) | g.degree(s.src) : 0ull;
   if (tid < GBG_MAX_LEVELS) s.level_examined[tid] = 0;
-  grid.sync();
   if (tid == 0) {
-    const uint32_t bit = 1u << (s.src & 31);
-    s.visited[s.src >> 5] |= bit;
-    s.bm[0][s.src >> 5] |= bit;
-    s.depth[s.src] = 0;
     s.list[0][0] = s.src;
-    const uint32_t d = g.degree(s.src);
     s.dscan[0][0] = 0;
-    s.packed[0] = (1ull << kPackShift) | d;
     s.level_ns[0] = globaltimer();
   }
   grid.sync();
@@ -349,30 +345,32 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.bm[1] = tb.b.bm;
   s.bm[2] = g->ws.get<uint32_t>("bfs.bm2", tb.nw + 2);
   s.packed = g->ws.get<unsigned long long>("bfs.ring", 4);
-  uint64_t* stat = g->ws.get<uint64_t>("bfs.stat", 3 * GBG_MAX_LEVELS + 8);
+  // every per-level statistic in one block, read back with one copy into
+  // the handle's pinned staging: [packed | ns (+1) | result (2) | examined | modes]
+  constexpr int ML = GBG_MAX_LEVELS;
+  constexpr size_t kStatWords = 3 * ML + 4 + ML / 2;
+  static_assert(kStatWords * sizeof(uint64_t) <= kHostScalarBytes, "BFS stats exceed the pinned staging");
+  uint64_t* stat = g->ws.get<uint64_t>("bfs.stat", kStatWords);
   s.level_packed = stat;
-  s.level_ns = reinterpret_cast<unsigned long long*>(stat + GBG_MAX_LEVELS);
-  s.result = stat + 2 * GBG_MAX_LEVELS + 2;
-  s.level_mode = g->ws.get<int32_t>("bfs.modes", GBG_MAX_LEVELS);
+  s.level_ns = reinterpret_cast<unsigned long long*>(stat + ML);
+  s.result = stat + 2 * ML + 2;
+  s.level_examined = reinterpret_cast<unsigned long long*>(stat + 2 * ML + 4);
+  s.level_mode = reinterpret_cast<int32_t*>(stat + 3 * ML + 4);
   s.blocksum = g->ws.get<uint64_t>("bfs.blocksum", grid);
   s.nw = tb.nw;
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
   s.src = src;
   s.first = first_neighbors(g);
   s.iso = isolated_bitmap(g);
-  s.level_examined = g->ws.get<unsigned long long>("bfs.examined", GBG_MAX_LEVELS);
   void* args[] = {&view, &s};
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));
   g->launches++;
-  std::vector<uint64_t> hs(3 * GBG_MAX_LEVELS + 8);
-  std::vector<int32_t> hm(GBG_MAX_LEVELS);
-  std::vector<unsigned long long> hx(GBG_MAX_LEVELS);
-  GBG_CUDA(cudaMemcpyAsync(hs.data(), stat, hs.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
-  GBG_CUDA(cudaMemcpyAsync(hx.data(), s.level_examined, hx.size() * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, g->stream));
-  GBG_CUDA(cudaMemcpyAsync(hm.data(), s.level_mode, hm.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+  GBG_CUDA(cudaMemcpyAsync(g->hscalar, stat, kStatWords * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
   GBG_CUDA(cudaStreamSynchronize(g->stream));
+  const uint64_t* hs = g->hscalar;
+  const unsigned long long* hx = reinterpret_cast<const unsigned long long*>(hs + 2 * ML + 4);
+  const int32_t* hm = reinterpret_cast<const int32_t*>(hs + 3 * ML + 4);
   if (st) {
     std::memset(st, 0, sizeof(*st));
     const uint64_t levels = hs[2 * GBG_MAX_LEVELS + 2];

@@ -153,6 +153,10 @@ struct TcCache;     // tc.cu
 
 }  // namespace gbg
 
+namespace gbg {
+constexpr size_t kHostScalarBytes = 4096;  // gbg_graph::hscalar
+}  // namespace gbg
+
 struct gbg_graph {
   int kind = GBG_KIND_CSR;
   int device = 0;
@@ -193,7 +197,7 @@ struct gbg_graph {
   gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
 
   gbg::Workspace ws;
-  // pinned host staging for small device->host scalars
+  // pinned host staging for small device->host reads (scalars, per-level stats)
   uint64_t* hscalar = nullptr;
 
   gbg::CsrView csr_view() const { return {n, off, nbr}; }
