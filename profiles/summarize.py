@@ -2,6 +2,7 @@
 
     python profiles/summarize.py full   <report.ncu-rep> <out.md> [--json profiles/ncu_summary.json]
     python profiles/summarize.py launches <launches.csv>  <out.md>
+    python profiles/summarize.py lines  <report.ncu-rep> <out.md>
 
 `full` reads one `ncu --set full` capture (raw page) and writes the metrics
 the roofline uses (duration, DRAM bytes, L2/L1 hit rates and throughputs,
@@ -116,9 +117,36 @@ def launches(csv_path, out_md):
         f.write("\n".join(lines) + "\n")
 
 
+def lines(rep, out_md, top=30):
+    """Warp-stall samples per CUDA source line (inlined frames attributed to
+    each line they pass through, so shares overlap across nesting levels)."""
+    r = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                       capture_output=True, text=True, check=True)
+    cur, rows = None, []
+    for rec in csv.reader(r.stdout.splitlines()):
+        if not rec:
+            continue
+        if rec[0] == "File Path":
+            cur = os.path.basename(rec[1])
+        elif len(rec) > 5 and rec[0].isdigit() and rec[2] == "-":
+            try:
+                rows.append((int(rec[4]), cur, int(rec[0]), rec[1].strip()[:100]))
+            except ValueError:
+                pass
+    tot = sum(x[0] for x in rows) or 1
+    out = [f"# warp-stall samples by source line: {os.path.basename(rep)}", "",
+           "| share | samples | line | source |", "|---|---|---|---|"]
+    for smp, f, ln, src in sorted(rows, reverse=True)[:top]:
+        out.append(f"| {100 * smp / tot:.1f}% | {smp} | {f}:{ln} | `{src.replace('|', '/')}` |")
+    with open(out_md, "w") as fh:
+        fh.write("\n".join(out) + "\n")
+
+
 if __name__ == "__main__":
     mode = sys.argv[1]
-    if mode == "full":
+    if mode == "lines":
+        lines(sys.argv[2], sys.argv[3])
+    elif mode == "full":
         jp = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
         full(sys.argv[2], sys.argv[3], jp)
     else:
