@@ -307,10 +307,11 @@ __device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { r
 constexpr uint32_t kNoFirst = 0xffffffffu;
 
 // Early-exit pull for operators whose cond is a bitmap (Op::cond_word(w):
-// the 32 cond bits of word w).  Each warp owns a contiguous run of words and
-// reads their cond words 32 at a time in one coalesced load, so a word's
-// dependent chain starts at first[] / the row bounds instead of at its cond
-// word, and words without a live vertex cost nothing.
+// the 32 cond bits of word w).  Each warp takes batches of up to 8 words and
+// reads a batch's cond words in one coalesced load, so a word's dependent
+// chain starts at first[] / the row bounds instead of at its cond word, and
+// words without a live vertex cost nothing.
+constexpr uint64_t kCwBatch = 8;
 template <class G, class Op>
 __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
                                               unsigned long long* packed, const uint32_t* first,
@@ -318,11 +319,15 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  // strided batches of B words (B <= kCwBatch): a warp's batches spread
+  // over the whole id range, which balances the per-word work (static
+  // contiguous runs left a 10-40 us tail of late CTAs before the barrier;
+  // a shared batch counter costs more in contention than it recovers)
   const uint64_t per = (nwords + nwarps - 1) / nwarps;
-  const uint64_t wbeg = gwarp * per;
-  const uint64_t wend = wbeg + per < nwords ? wbeg + per : nwords;
+  const uint64_t B = per < kCwBatch ? (per ? per : 1) : kCwBatch;
   unsigned long long cnt = 0, degsum = 0, ex = 0;
-  for (uint64_t wb = wbeg; wb < wend; wb += 32) {
+  for (uint64_t wb = gwarp * B; wb < nwords; wb += nwarps * B) {
+    const uint64_t wend = wb + B < nwords ? wb + B : nwords;
     const uint64_t wl = wb + lane;
     uint32_t cw = 0;
     if (wl < wend) {
