@@ -60,16 +60,48 @@ __global__ void offsets_from_sorted64_k(const uint32_t* src, uint64_t m, uint64_
   }
 }
 
-__device__ __forceinline__ bool bsearch_u32(const uint32_t* a, uint32_t len, uint32_t x) {
-  uint32_t lo = 0, hi = len;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    uint32_t y = __ldg(a + mid);
-    if (y < x) lo = mid + 1;
-    else if (y > x) hi = mid;
-    else return true;
+// first index i in [lo, len) with a[i] >= x: exponential probes from lo,
+// then a binary search inside the bracket.  The elements of the shorter list
+// are searched in increasing order, so each search starts where the last
+// one ended and costs O(log gap) instead of O(log len).
+__device__ __forceinline__ uint32_t gallop_lb(const uint32_t* a, uint32_t lo, uint32_t len, uint32_t x) {
+  uint32_t r, step = 1;
+  for (;;) {
+    const uint32_t p = lo + step - 1;
+    if (p >= len) {
+      r = len;
+      break;
+    }
+    if (__ldg(a + p) >= x) {
+      r = p;
+      break;
+    }
+    lo = p + 1;
+    step <<= 1;
   }
-  return false;
+  while (lo < r) {
+    const uint32_t mid = (lo + r) >> 1;
+    if (__ldg(a + mid) < x) lo = mid + 1; else r = mid;
+  }
+  return lo;
+}
+
+// |{a[i] : i = first, first + stride, ...} ∩ b| for ascending a and b
+__device__ __forceinline__ uint32_t count_common(const uint32_t* a, uint32_t la, const uint32_t* b, uint32_t lb,
+                                                 uint32_t first, uint32_t stride) {
+  if (!lb) return 0;
+  const uint32_t bmax = __ldg(b + lb - 1);
+  uint32_t c = 0, pos = 0;
+  for (uint32_t i = first; i < la; i += stride) {
+    const uint32_t x = __ldg(a + i);
+    if (x > bmax) break;
+    pos = gallop_lb(b, pos, lb, x);
+    if (pos < lb && __ldg(b + pos) == x) {
+      ++c;
+      ++pos;
+    }
+  }
+  return c;
 }
 
 __global__ void __launch_bounds__(256) tc_count_k(uint64_t mo, const uint64_t* __restrict__ ooff,
@@ -95,8 +127,7 @@ __global__ void __launch_bounds__(256) tc_count_k(uint64_t mo, const uint64_t* _
       la = du <= dv ? du : dv;
       lb = du <= dv ? dv : du;
     }
-    if (la <= 32)
-      for (uint32_t i = 0; i < la; ++i) cnt += bsearch_u32(b, lb, __ldg(a + i));
+    if (la <= 32) cnt += count_common(a, la, b, lb, 0, 1);
     uint32_t hard = __ballot_sync(0xffffffffu, la > 32);
     while (hard) {
       const int l = __ffs(hard) - 1;
@@ -104,7 +135,7 @@ __global__ void __launch_bounds__(256) tc_count_k(uint64_t mo, const uint64_t* _
       const uint32_t* aa = reinterpret_cast<const uint32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(a), l));
       const uint32_t* bb = reinterpret_cast<const uint32_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(b), l));
       const uint32_t na = __shfl_sync(0xffffffffu, la, l), nb = __shfl_sync(0xffffffffu, lb, l);
-      for (uint32_t i = lane; i < na; i += 32) cnt += bsearch_u32(bb, nb, __ldg(aa + i));
+      cnt += count_common(aa, na, bb, nb, lane, 32);
     }
   }
   cnt = block_sum(cnt, s_red);
