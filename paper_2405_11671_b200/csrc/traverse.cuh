@@ -306,11 +306,76 @@ __device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { r
 // 82% of the unvisited vertices with edges hit on their first neighbour).
 constexpr uint32_t kNoFirst = 0xffffffffu;
 
+// One vertex of an early-exit pull per lane (c = the lane holds a live
+// vertex v): the cached first neighbour, then up to kPullSerial list
+// entries by the lane itself, then the whole warp 32 entries per step for
+// each lane still unresolved (ballot on frontier hits, the first hit in
+// list order wins).  Warp-uniform entry; returns whether v was reached and
+// its degree in d.
+template <class G, class Op>
+__device__ __forceinline__ bool pull_vertex(G g, const uint32_t* fb, Op op, const uint32_t* first, bool c, uint32_t v,
+                                            uint32_t& d, unsigned long long& ex) {
+  const int lane = threadIdx.x & 31;
+  uint64_t b = 0;
+  d = 0;
+  bool found = false;
+  uint32_t lim = 0;
+  if (c) {
+    const uint32_t f = __ldg(first + v);
+    g.seg(v, b, d);
+    if (f != kNoFirst && frontier_bit(fb, f) && op.update(f, v)) found = true;
+    ex += d ? 1 : 0;
+    lim = found ? 0 : (d < kPullSerial ? d : kPullSerial);
+  }
+  for (uint32_t k = 1; k < lim; ++k) {
+    const uint32_t u = g.at(b + k);
+    ++ex;
+    if (frontier_bit(fb, u) && op.update(u, v)) {
+      found = true;
+      break;
+    }
+  }
+  uint32_t hard = __ballot_sync(0xffffffffu, c && d > kPullSerial && !found);
+  while (hard) {
+    const int l = __ffs(hard) - 1;
+    hard &= hard - 1;
+    const uint64_t bb = __shfl_sync(0xffffffffu, b, l);
+    const uint32_t dd = __shfl_sync(0xffffffffu, d, l);
+    const uint32_t vv = __shfl_sync(0xffffffffu, v, l);
+    bool fl = false;
+    for (uint32_t j0 = kPullSerial; j0 < dd; j0 += 32) {
+      const uint32_t jj = j0 + lane;
+      uint32_t u = 0;
+      const bool hit = jj < dd && frontier_bit(fb, u = g.at(bb + jj));
+      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      if (!hm) continue;
+      const int fi = __ffs(hm) - 1;
+      bool r = false;
+      if (lane == fi) r = op.update(u, vv);
+      if (__shfl_sync(0xffffffffu, r, fi)) {
+        fl = true;
+        if (lane == l) ex += j0 + fi + 1 - kPullSerial;
+        break;
+      }
+    }
+    if (lane == l) {
+      if (fl) found = true;
+      else ex += dd - kPullSerial;
+    }
+  }
+  return found;
+}
+
 // Early-exit pull for operators whose cond is a bitmap (Op::cond_word(w):
 // the 32 cond bits of word w).  Each warp takes batches of up to 8 words and
 // reads a batch's cond words in one coalesced load, so a word's dependent
 // chain starts at first[] / the row bounds instead of at its cond word, and
-// words without a live vertex cost nothing.
+// words without a live vertex cost nothing.  A batch with at most 32 live
+// vertices (sparse cond, e.g. the second dense BFS level) is packed onto
+// the lanes and resolved in one round, one dependent chain for the whole
+// batch, each word's found bits reassembled with a warp OR-reduction;
+// denser batches run word by word, lane = vertex (scale 24: level 2
+// 76 -> 46 us; the packed form for dense batches cost level 1 30%).
 constexpr uint64_t kCwBatch = 8;
 template <class G, class Op>
 __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
@@ -324,7 +389,7 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
   // contiguous runs left a 10-40 us tail of late CTAs before the barrier;
   // a shared batch counter costs more in contention than it recovers)
   const uint64_t per = (nwords + nwarps - 1) / nwarps;
-  const uint64_t B = per < kCwBatch ? (per ? per : 1) : kCwBatch;
+  const uint32_t B = static_cast<uint32_t>(per < kCwBatch ? (per ? per : 1) : kCwBatch);
   unsigned long long cnt = 0, degsum = 0, ex = 0;
   for (uint64_t wb = gwarp * B; wb < nwords; wb += nwarps * B) {
     const uint64_t wend = wb + B < nwords ? wb + B : nwords;
@@ -334,68 +399,62 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
       cw = op.cond_word(wl);
       if (wl * 32 + 32 > g.n) cw &= g.n > wl * 32 ? (1u << (g.n - wl * 32)) - 1u : 0u;
     }
+    const uint32_t pc = __popc(cw);
+    const uint32_t excl = warp_inclusive_scan(pc) - pc;
+    const uint32_t total = __shfl_sync(0xffffffffu, excl + pc, 31);
+    if (total <= 32) {
+      // packed: lane t takes the t-th live vertex of the batch
+      const bool c = static_cast<uint32_t>(lane) < total;
+      uint32_t j = 0, ej = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < kCwBatch; ++k) {
+        const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
+        if (k < B && ek <= static_cast<uint32_t>(lane)) {
+          j = k;
+          ej = ek;
+        }
+      }
+      const uint32_t cwj = __shfl_sync(0xffffffffu, cw, j);
+      const uint32_t bit = c ? __fns(cwj, 0, static_cast<int>(lane - ej + 1)) : 0u;
+      const uint32_t v = static_cast<uint32_t>((wb + j) * 32 + bit);
+      uint32_t d;
+      const bool found = total && pull_vertex(g, fb, op, first, c, v, d, ex);
+      const uint32_t mine = found ? 1u << bit : 0u;
+      uint32_t fword = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < kCwBatch; ++k) {
+        if (k >= B) break;
+        const uint32_t m = __reduce_or_sync(0xffffffffu, j == k ? mine : 0u);
+        if (lane == static_cast<int>(k)) fword = m;
+      }
+      if (found) {
+        ++cnt;
+        degsum += d;
+      }
+      if (wl < wend) {
+        nb[wl] = fword;
+        if (fword) op.dense_word(wl, fword);
+      }
+      continue;
+    }
     if (wl < wend && !cw) nb[wl] = 0;
     uint32_t live = __ballot_sync(0xffffffffu, cw != 0);
     while (live) {
       const int j = __ffs(live) - 1;
       live &= live - 1;
       const uint64_t w = wb + j;
-      const uint32_t v = static_cast<uint32_t>(w * 32 + lane);
       const bool c = (__shfl_sync(0xffffffffu, cw, j) >> lane) & 1u;
-      uint64_t b = 0;
-      uint32_t d = 0;
-      bool found = false;
-      uint32_t lim = 0;
-      if (c) {
-        const uint32_t f = __ldg(first + v);
-        g.seg(v, b, d);
-        if (f != kNoFirst && frontier_bit(fb, f) && op.update(f, v)) found = true;
-        ex += d ? 1 : 0;
-        lim = found ? 0 : (d < kPullSerial ? d : kPullSerial);
-      }
-      for (uint32_t k = 1; k < lim; ++k) {
-        const uint32_t u = g.at(b + k);
-        ++ex;
-        if (frontier_bit(fb, u) && op.update(u, v)) {
-          found = true;
-          break;
-        }
-      }
-      uint32_t hard = __ballot_sync(0xffffffffu, c && d > kPullSerial && !found);
-      while (hard) {
-        const int l = __ffs(hard) - 1;
-        hard &= hard - 1;
-        const uint64_t bb = __shfl_sync(0xffffffffu, b, l);
-        const uint32_t dd = __shfl_sync(0xffffffffu, d, l);
-        const uint32_t vv = static_cast<uint32_t>(w * 32 + l);
-        bool fl = false;
-        for (uint32_t j0 = kPullSerial; j0 < dd; j0 += 32) {
-          const uint32_t jj = j0 + lane;
-          uint32_t u = 0;
-          const bool hit = jj < dd && frontier_bit(fb, u = g.at(bb + jj));
-          const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-          if (!hm) continue;
-          const int fi = __ffs(hm) - 1;
-          bool r = false;
-          if (lane == fi) r = op.update(u, vv);
-          if (__shfl_sync(0xffffffffu, r, fi)) {
-            fl = true;
-            if (lane == l) ex += j0 + fi + 1 - kPullSerial;
-            break;
-          }
-        }
-        if (lane == l) {
-          if (fl) found = true;
-          else ex += dd - kPullSerial;
-        }
-      }
+      uint32_t d;
+      const bool found = pull_vertex(g, fb, op, first, c, static_cast<uint32_t>(w * 32 + lane), d, ex);
       const uint32_t fm = __ballot_sync(0xffffffffu, found);
       if (lane == 0) {
         nb[w] = fm;
         if (fm) op.dense_word(w, fm);
       }
-      cnt += __popc(fm) * (lane == 0);
-      if (found) degsum += d;
+      if (found) {
+        ++cnt;
+        degsum += d;
+      }
     }
   }
   cnt = warp_sum(cnt);
