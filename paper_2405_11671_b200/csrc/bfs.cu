@@ -19,6 +19,10 @@
 
 #include "traverse.cuh"
 
+#ifndef GBG_BFS_MINB
+#define GBG_BFS_MINB 5
+#endif
+
 namespace gbg {
 
 // BFS as an edge_map operator: cond = unvisited, claim = atomic test-and-set
@@ -99,9 +103,11 @@ struct CoopState {
   uint64_t nw;
   double threshold;            // (1/20) * m, evaluated on the host like traversal.cpp:105-106
   uint32_t src;
-  const uint32_t* first;       // first neighbours (dense-level shortcut)
+  const uint64_t* first;       // (degree << 32) | first neighbour (dense-level shortcut)
   const uint32_t* iso;         // isolated vertices: pre-set in `visited` (never reached, never pulled)
   unsigned long long* level_examined;  // [GBG_MAX_LEVELS] arcs inspected by dense levels
+  unsigned* level_heavy;       // [GBG_MAX_LEVELS] a dense level reached a vertex of degree > kBitmapPushMaxDeg
+  int bitmap_push;             // dense -> sparse transitions push straight from the bitmap
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -141,7 +147,7 @@ __device__ void coop_bitmap_to_list(cooperative_groups::grid_group& grid, G g, c
 }
 
 template <class G>
-__global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) {
+__global__ void __launch_bounds__(kPushThreads, GBG_BFS_MINB) bfs_coop_k(G g, CoopState s) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   __shared__ uint32_t s_idx[kPushTile];
   __shared__ uint64_t s_red[33];
@@ -157,7 +163,10 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     s.bm[1][w] = 0;
   }
   if (tid < 3) s.packed[tid] = tid == 0 ? (1ull << kPackShift) | g.degree(s.src) : 0ull;
-  if (tid < GBG_MAX_LEVELS) s.level_examined[tid] = 0;
+  if (tid < GBG_MAX_LEVELS) {
+    s.level_examined[tid] = 0;
+    s.level_heavy[tid] = 0;
+  }
   if (tid == 0) {
     s.list[0][0] = s.src;
     s.dscan[0][0] = 0;
@@ -192,8 +201,15 @@ __global__ void __launch_bounds__(kPushThreads, 8) bfs_coop_k(G g, CoopState s) 
     for (uint64_t w = tid; w < s.nw; w += nthreads) s.bm[bclr][w] = 0;
     if (dense) {
       pull_words<G, BfsOp, true>(g, s.bm[bcur], op, s.bm[bnxt], s.nw, acc, s.first,
-                                 level <= GBG_MAX_LEVELS ? s.level_examined + level - 1 : nullptr);
+                                 level <= GBG_MAX_LEVELS ? s.level_examined + level - 1 : nullptr,
+                                 level <= GBG_MAX_LEVELS ? s.level_heavy + level - 1 : nullptr);
       has_list = false;
+    } else if (!has_list && s.bitmap_push && level - 1 <= GBG_MAX_LEVELS &&
+               !*reinterpret_cast<volatile unsigned*>(s.level_heavy + level - 2)) {
+      // dense -> sparse with no member above kBitmapPushMaxDeg: push from
+      // the bitmap, no list to build first
+      push_bitmap(g, s.bm[bcur], s.nw, op, s.list[nxt], s.dscan[nxt], s.bm[bnxt], acc);
+      has_list = true;
     } else {
       if (!has_list) {
         coop_bitmap_to_list(grid, g, s.bm[bcur], s.nw, s.list[cur], s.dscan[cur], s.blocksum, s_red);
@@ -285,7 +301,7 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
       cur.has_bm = true;
     }
     GBG_LAUNCH(g, (pull_k<G, Op, kEarly>), pull_grid(g, tb.nw), kPullThreads, 0, view, cur.bm, op, out.bm, tb.nw,
-               tb.packed, kEarly ? first_neighbors(g) : static_cast<const uint32_t*>(nullptr), examined);
+               tb.packed, kEarly ? first_neighbors(g) : static_cast<const uint64_t*>(nullptr), examined);
     out.has_bm = true;
   } else {
     ensure_list(g, view, tb, cur);
@@ -307,7 +323,7 @@ void edge_map_step(gbg_graph* g, G view, TraversalBuffers& tb, Frontier& cur, Fr
 
 // first neighbour of every vertex, and the bitmap of isolated vertices
 template <class G>
-__global__ void first_nbr_k(G g, uint32_t* first, uint32_t* iso) {
+__global__ void first_nbr_k(G g, uint64_t* first, uint32_t* iso) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~uint64_t{31}; base < g.n;
        base += stride) {
@@ -317,12 +333,23 @@ __global__ void first_nbr_k(G g, uint32_t* first, uint32_t* iso) {
       uint64_t b;
       uint32_t d;
       g.seg(static_cast<uint32_t>(v), b, d);
-      first[v] = d ? g.at(b) : kNoFirst;
+      first[v] = (static_cast<uint64_t>(d) << 32) | (d ? g.at(b) : kNoFirst);
       isolated = d == 0;
     }
     const uint32_t m = __ballot_sync(0xffffffffu, isolated);
     if ((threadIdx.x & 31) == 0) iso[base >> 5] = m;
   }
+}
+
+// GBG_BFS_BITMAP_PUSH=0 turns the bitmap-driven push of dense -> sparse
+// transitions off (the list is then built first, as the launch-per-level
+// path does); a comparison and test knob.
+bool bitmap_push_enabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("GBG_BFS_BITMAP_PUSH");
+    return e && e[0] == '0';
+  }();
+  return !off;
 }
 
 // The persistent path; false when the device cannot co-schedule the grid.
@@ -356,6 +383,8 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.result = stat + 2 * ML + 2;
   s.level_examined = reinterpret_cast<unsigned long long*>(stat + 2 * ML + 4);
   s.level_mode = reinterpret_cast<int32_t*>(stat + 3 * ML + 4);
+  s.level_heavy = g->ws.get<unsigned>("bfs.heavy", ML);
+  s.bitmap_push = bitmap_push_enabled();
   s.blocksum = g->ws.get<uint64_t>("bfs.blocksum", grid);
   s.nw = tb.nw;
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
@@ -531,18 +560,20 @@ void bc_run(gbg_graph* g, G view, uint32_t src, double* delta) {
 }  // namespace gbg
 
 namespace gbg {
-const uint32_t* first_neighbors(gbg_graph* g) {
+const uint64_t* first_neighbors(gbg_graph* g) {
   const uint64_t nw = (g->n + 31) / 32;
-  if (!g->first) g->first = dalloc<uint32_t>(g->n + nw + 1);  // ids, then the isolated bitmap
+  // (degree, first) words, then the isolated bitmap
+  if (!g->first) g->first = dalloc<uint64_t>(g->n + nw / 2 + 1);
   if (!g->first_valid) {
     with_view(g, [&](auto view) {
-      GBG_LAUNCH(g, first_nbr_k<decltype(view)>, grid_for(nw * 32, 256), 256, 0, view, g->first, g->first + g->n);
+      GBG_LAUNCH(g, first_nbr_k<decltype(view)>, grid_for(nw * 32, 256), 256, 0, view, g->first,
+                 reinterpret_cast<uint32_t*>(g->first + g->n));
     });
     g->first_valid = true;
   }
   return g->first;
 }
-const uint32_t* isolated_bitmap(gbg_graph* g) { return first_neighbors(g) + g->n; }
+const uint32_t* isolated_bitmap(gbg_graph* g) { return reinterpret_cast<const uint32_t*>(first_neighbors(g) + g->n); }
 }  // namespace gbg
 
 using namespace gbg;

@@ -192,7 +192,7 @@ struct gbg_graph {
   // derived, rebuilt lazily after updates
   uint64_t* voff = nullptr;    // exclusive scan of degrees (blocked only)
   bool voff_valid = false;
-  uint32_t* first = nullptr;   // first neighbour of every vertex (kNoFirst if isolated) + isolated bitmap
+  uint64_t* first = nullptr;   // (degree << 32) | first neighbour of every vertex (kNoFirst if isolated) + isolated bitmap
   bool first_valid = false;
   gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
 
@@ -261,9 +261,9 @@ inline bool coop_enabled(int device) {
   return coop != 0;
 }
 
-// Every vertex's first neighbour (traverse.cuh kNoFirst when isolated),
+// Every vertex's (degree << 32) | first neighbour (traverse.cuh kNoFirst when isolated),
 // kept until the next update (bfs.cu).
-const uint32_t* first_neighbors(gbg_graph* g);
+const uint64_t* first_neighbors(gbg_graph* g);
 // Bit v set when v has no neighbours (same lifetime as first_neighbors).
 const uint32_t* isolated_bitmap(gbg_graph* g);
 

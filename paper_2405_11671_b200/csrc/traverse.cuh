@@ -25,6 +25,13 @@
 
 #include "scan.cuh"
 
+#ifndef GBG_PB_INLINE
+#define GBG_PB_INLINE __forceinline__
+#endif
+#ifndef GBG_PW_INLINE
+#define GBG_PW_INLINE __forceinline__
+#endif
+
 namespace gbg {
 
 __device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t v) {
@@ -291,6 +298,9 @@ __global__ void select_k(G g, Pred pred, uint32_t* list, uint64_t* dscan, unsign
 // ---------------------------------------------------------------- pull
 constexpr int kPullThreads = 256;
 constexpr uint32_t kPullSerial = 8;  // neighbours a lane scans before the warp helps
+// largest member degree a bitmap-driven push (push_bitmap) takes on: one
+// warp walks such a list 32 entries per step
+constexpr uint32_t kBitmapPushMaxDeg = 1024;
 
 // One warp per 32-vertex bitmap word (so output / visited words need no
 // atomics).  Each lane first scans up to kPullSerial neighbours of its own
@@ -306,14 +316,29 @@ __device__ __forceinline__ bool frontier_bit(const uint32_t* bm, uint32_t v) { r
 // 82% of the unvisited vertices with edges hit on their first neighbour).
 constexpr uint32_t kNoFirst = 0xffffffffu;
 
+constexpr uint64_t kCwBatch = 8;  // words per warp batch of the bitmap-driven loops
+#ifndef GBG_PH1
+#define GBG_PH1 4
+#endif
+constexpr uint32_t kPh1 = GBG_PH1;  // words whose first-neighbour tests are in flight at once
+
+// The first-neighbour table of early-exit pulls: per vertex one 64-bit word
+// (degree << 32) | first neighbour (first = kNoFirst when isolated), so one
+// coalesced 8-byte load gives both the test that settles most vertices of a
+// dense level and the degree the next frontier's degree sum needs; the row
+// offsets are read only for vertices that miss.
+__device__ __forceinline__ uint32_t fd_first(uint64_t x) { return static_cast<uint32_t>(x); }
+__device__ __forceinline__ uint32_t fd_deg(uint64_t x) { return static_cast<uint32_t>(x >> 32); }
+
 // One vertex of an early-exit pull per lane (c = the lane holds a live
-// vertex v): the cached first neighbour, then up to kPullSerial list
-// entries by the lane itself, then the whole warp 32 entries per step for
-// each lane still unresolved (ballot on frontier hits, the first hit in
-// list order wins).  Warp-uniform entry; returns whether v was reached and
-// its degree in d.
-template <class G, class Op>
-__device__ __forceinline__ bool pull_vertex(G g, const uint32_t* fb, Op op, const uint32_t* first, bool c, uint32_t v,
+// vertex v).  kFirst: test the cached first neighbour first (counted in
+// ex); otherwise v is known to have missed there and to have d > 1.  Then
+// up to kPullSerial list entries by the lane itself, then the whole warp 32
+// entries per step for each lane still unresolved (ballot on frontier hits,
+// the first hit in list order wins).  Warp-uniform entry; returns whether
+// v was reached, its degree in d.
+template <bool kFirst, class G, class Op>
+__device__ __forceinline__ bool pull_vertex(G g, const uint32_t* fb, Op op, const uint64_t* fd, bool c, uint32_t v,
                                             uint32_t& d, unsigned long long& ex) {
   const int lane = threadIdx.x & 31;
   uint64_t b = 0;
@@ -321,11 +346,16 @@ __device__ __forceinline__ bool pull_vertex(G g, const uint32_t* fb, Op op, cons
   bool found = false;
   uint32_t lim = 0;
   if (c) {
-    const uint32_t f = __ldg(first + v);
-    g.seg(v, b, d);
-    if (f != kNoFirst && frontier_bit(fb, f) && op.update(f, v)) found = true;
-    ex += d ? 1 : 0;
-    lim = found ? 0 : (d < kPullSerial ? d : kPullSerial);
+    if (kFirst) {
+      const uint64_t x = __ldg(fd + v);
+      d = fd_deg(x);
+      if (d && frontier_bit(fb, fd_first(x)) && op.update(fd_first(x), v)) found = true;
+      ex += d ? 1 : 0;
+    }
+    if (!found) {
+      g.seg(v, b, d);
+      lim = d < kPullSerial ? d : kPullSerial;
+    }
   }
   for (uint32_t k = 1; k < lim; ++k) {
     const uint32_t u = g.at(b + k);
@@ -366,21 +396,42 @@ __device__ __forceinline__ bool pull_vertex(G g, const uint32_t* fb, Op op, cons
   return found;
 }
 
+// Hand out the set bits of the lanes' words (lane k < B holds word wb + k
+// in `w`, exclusive prefix of the popcounts in `excl`) to the lanes: lane
+// t of round r0 gets bit number r0 + t; returns its word index j and bit.
+__device__ __forceinline__ void packed_bit(uint32_t w, uint32_t excl, uint32_t B, uint32_t t, uint32_t& j,
+                                           uint32_t& bit) {
+  uint32_t ej = 0;
+  j = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kCwBatch; ++k) {
+    const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
+    if (k < B && ek <= t) {
+      j = k;
+      ej = ek;
+    }
+  }
+  const uint32_t wj = __shfl_sync(0xffffffffu, w, j);
+  bit = __fns(wj, 0, static_cast<int>(t - ej + 1));
+}
+
 // Early-exit pull for operators whose cond is a bitmap (Op::cond_word(w):
-// the 32 cond bits of word w).  Each warp takes batches of up to 8 words and
-// reads a batch's cond words in one coalesced load, so a word's dependent
-// chain starts at first[] / the row bounds instead of at its cond word, and
-// words without a live vertex cost nothing.  A batch with at most 32 live
-// vertices (sparse cond, e.g. the second dense BFS level) is packed onto
-// the lanes and resolved in one round, one dependent chain for the whole
-// batch, each word's found bits reassembled with a warp OR-reduction;
-// denser batches run word by word, lane = vertex (scale 24: level 2
-// 76 -> 46 us; the packed form for dense batches cost level 1 30%).
-constexpr uint64_t kCwBatch = 8;
+// the 32 cond bits of word w).  Each warp takes strided batches of up to 8
+// words and reads a batch's cond words in one coalesced load.
+//  * A batch with at most 32 live vertices (sparse cond, e.g. the second
+//    dense BFS level) is packed onto the lanes and resolved in one round:
+//    one dependent chain for the whole batch.
+//  * Denser batches run in two phases: the first-neighbour test of every
+//    live vertex, four words' (first, degree) loads and then four words'
+//    frontier-bit loads in flight at once; then the vertices that missed
+//    (18% at scale 24 level 1) packed onto the lanes, 32 per round, for
+//    the list scan from entry 1.
+// Each word's found bits are reassembled with warp OR-reductions; the
+// owning warp writes the output word and publishes the visited bits.
 template <class G, class Op>
 __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
-                                              unsigned long long* packed, const uint32_t* first,
-                                              unsigned long long* examined) {
+                                              unsigned long long* packed, const uint64_t* fd,
+                                              unsigned long long* examined, unsigned* heavy) {
   const int lane = threadIdx.x & 31;
   const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -391,6 +442,7 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
   const uint64_t per = (nwords + nwarps - 1) / nwarps;
   const uint32_t B = static_cast<uint32_t>(per < kCwBatch ? (per ? per : 1) : kCwBatch);
   unsigned long long cnt = 0, degsum = 0, ex = 0;
+  bool big = false;
   for (uint64_t wb = gwarp * B; wb < nwords; wb += nwarps * B) {
     const uint64_t wend = wb + B < nwords ? wb + B : nwords;
     const uint64_t wl = wb + lane;
@@ -399,64 +451,81 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
       cw = op.cond_word(wl);
       if (wl * 32 + 32 > g.n) cw &= g.n > wl * 32 ? (1u << (g.n - wl * 32)) - 1u : 0u;
     }
-    const uint32_t pc = __popc(cw);
-    const uint32_t excl = warp_inclusive_scan(pc) - pc;
-    const uint32_t total = __shfl_sync(0xffffffffu, excl + pc, 31);
-    if (total <= 32) {
-      // packed: lane t takes the t-th live vertex of the batch
-      const bool c = static_cast<uint32_t>(lane) < total;
-      uint32_t j = 0, ej = 0;
+    uint32_t pc = __popc(cw);
+    uint32_t excl = warp_inclusive_scan(pc) - pc;
+    uint32_t total = __shfl_sync(0xffffffffu, excl + pc, 31);
+    uint32_t fword = 0;  // lane k < B: found bits of word wb + k
+    uint32_t todo = cw;  // lane k < B: live bits of word wb + k still to resolve
+    bool first_done = false;
+    if (total > 32) {
+      // phase 1: first-neighbour tests, 4 words at a time
+      uint32_t miss = 0;
+      for (uint32_t k0 = 0; k0 < B; k0 += kPh1) {
+        uint64_t x[kPh1];
+        bool c[kPh1];
 #pragma unroll
-      for (uint32_t k = 0; k < kCwBatch; ++k) {
-        const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
-        if (k < B && ek <= static_cast<uint32_t>(lane)) {
-          j = k;
-          ej = ek;
+        for (uint32_t q = 0; q < kPh1; ++q) {
+          c[q] = k0 + q < B && ((__shfl_sync(0xffffffffu, cw, (k0 + q) & 31) >> lane) & 1u);
+          x[q] = c[q] ? __ldg(fd + (wb + k0 + q) * 32 + lane) : 0ull;
+        }
+        bool h[kPh1];
+#pragma unroll
+        for (uint32_t q = 0; q < kPh1; ++q) h[q] = c[q] && fd_deg(x[q]) && frontier_bit(fb, fd_first(x[q]));
+#pragma unroll
+        for (uint32_t q = 0; q < kPh1; ++q) {
+          const uint32_t v = static_cast<uint32_t>((wb + k0 + q) * 32 + lane);
+          const uint32_t d = fd_deg(x[q]);
+          if (h[q] && !op.update(fd_first(x[q]), v)) h[q] = false;
+          ex += c[q] && d ? 1 : 0;
+          if (h[q]) {
+            ++cnt;
+            degsum += d;
+            big |= d > kBitmapPushMaxDeg;
+          }
+          const uint32_t fm = __ballot_sync(0xffffffffu, h[q]);
+          const uint32_t mm = __ballot_sync(0xffffffffu, c[q] && !h[q] && d > 1);
+          if (lane == static_cast<int>(k0 + q)) {
+            fword = fm;
+            miss = mm;
+          }
         }
       }
-      const uint32_t cwj = __shfl_sync(0xffffffffu, cw, j);
-      const uint32_t bit = c ? __fns(cwj, 0, static_cast<int>(lane - ej + 1)) : 0u;
+      todo = miss;
+      pc = __popc(todo);
+      excl = warp_inclusive_scan(pc) - pc;
+      total = __shfl_sync(0xffffffffu, excl + pc, 31);
+      first_done = true;
+    }
+    // packed rounds over the remaining live vertices
+    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+      const uint32_t t = r0 + lane;
+      const bool c = t < total;
+      uint32_t j, bit;
+      packed_bit(todo, excl, B, t, j, bit);
+      if (!c) bit = 0;
       const uint32_t v = static_cast<uint32_t>((wb + j) * 32 + bit);
       uint32_t d;
-      const bool found = total && pull_vertex(g, fb, op, first, c, v, d, ex);
+      const bool found = first_done ? pull_vertex<false>(g, fb, op, fd, c, v, d, ex)
+                                    : pull_vertex<true>(g, fb, op, fd, c, v, d, ex);
       const uint32_t mine = found ? 1u << bit : 0u;
-      uint32_t fword = 0;
 #pragma unroll
       for (uint32_t k = 0; k < kCwBatch; ++k) {
         if (k >= B) break;
         const uint32_t m = __reduce_or_sync(0xffffffffu, j == k ? mine : 0u);
-        if (lane == static_cast<int>(k)) fword = m;
+        if (lane == static_cast<int>(k)) fword |= m;
       }
       if (found) {
         ++cnt;
         degsum += d;
+        big |= d > kBitmapPushMaxDeg;
       }
-      if (wl < wend) {
-        nb[wl] = fword;
-        if (fword) op.dense_word(wl, fword);
-      }
-      continue;
     }
-    if (wl < wend && !cw) nb[wl] = 0;
-    uint32_t live = __ballot_sync(0xffffffffu, cw != 0);
-    while (live) {
-      const int j = __ffs(live) - 1;
-      live &= live - 1;
-      const uint64_t w = wb + j;
-      const bool c = (__shfl_sync(0xffffffffu, cw, j) >> lane) & 1u;
-      uint32_t d;
-      const bool found = pull_vertex(g, fb, op, first, c, static_cast<uint32_t>(w * 32 + lane), d, ex);
-      const uint32_t fm = __ballot_sync(0xffffffffu, found);
-      if (lane == 0) {
-        nb[w] = fm;
-        if (fm) op.dense_word(w, fm);
-      }
-      if (found) {
-        ++cnt;
-        degsum += d;
-      }
+    if (wl < wend) {
+      nb[wl] = fword;
+      if (fword) op.dense_word(wl, fword);
     }
   }
+  if (heavy && __any_sync(0xffffffffu, big) && lane == 0) *heavy = 1u;
   cnt = warp_sum(cnt);
   degsum = warp_sum(degsum);
   if (lane == 0 && cnt) atomicAdd(packed, (static_cast<unsigned long long>(cnt) << kPackShift) | degsum);
@@ -475,11 +544,11 @@ struct HasCondWord<Op, decltype(void(std::declval<const Op&>().cond_word(uint64_
 // inspect (up to and including the first hit under early exit).
 template <class G, class Op, bool kEarly>
 __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
-                                           unsigned long long* packed, const uint32_t* first = nullptr,
-                                           unsigned long long* examined = nullptr) {
+                                           unsigned long long* packed, const uint64_t* first = nullptr,
+                                           unsigned long long* examined = nullptr, unsigned* heavy = nullptr) {
   if constexpr (kEarly && HasCondWord<Op>::value) {
     if (first) {
-      pull_words_cw(g, fb, op, nb, nwords, packed, first, examined);
+      pull_words_cw(g, fb, op, nb, nwords, packed, first, examined, heavy);
       return;
     }
   }
@@ -497,9 +566,9 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
     if (c) {
       uint32_t j0 = 0;
       if (kEarly && first) {
-        const uint32_t f = __ldg(first + v);
+        const uint32_t f = fd_first(__ldg(first + v));
         g.seg(v, b, d);
-        if (f != kNoFirst && frontier_bit(fb, f) && op.update(f, v)) found = true;
+        if (d && frontier_bit(fb, f) && op.update(f, v)) found = true;
         j0 = 1;
         ex += d ? 1 : 0;
       } else {
@@ -565,8 +634,111 @@ __device__ __forceinline__ void pull_words(G g, const uint32_t* fb, Op op, uint3
 template <class G, class Op, bool kEarly>
 __global__ void __launch_bounds__(kPullThreads)
     pull_k(G g, const uint32_t* __restrict__ fb, Op op, uint32_t* __restrict__ nb, uint64_t nwords,
-           unsigned long long* packed, const uint32_t* __restrict__ first, unsigned long long* examined) {
+           unsigned long long* packed, const uint64_t* __restrict__ first, unsigned long long* examined) {
   pull_words<G, Op, kEarly>(g, fb, op, nb, nwords, packed, first, examined);
+}
+
+// ---------------------------------------------------------------- bitmap push
+// Warp-aggregated emission of the push output (as push_tile): one packed
+// atomic per warp step hands out list slots and degree-prefix offsets.
+template <class G>
+__device__ __forceinline__ void emit_warp(G g, bool emit, uint32_t v, uint32_t* out, uint64_t* out_dscan,
+                                          uint32_t* out_bm, unsigned long long* packed) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t mask = __ballot_sync(0xffffffffu, emit);
+  if (!mask) return;
+  const uint64_t dv = emit ? g.degree(v) : 0;
+  const uint64_t dinc = warp_inclusive_scan(dv);
+  const uint64_t dtot = __shfl_sync(0xffffffffu, dinc, 31);
+  const int leader = __ffs(mask) - 1;
+  unsigned long long old = 0;
+  if (lane == leader) old = atomicAdd(packed, (static_cast<unsigned long long>(__popc(mask)) << kPackShift) | dtot);
+  old = __shfl_sync(0xffffffffu, old, leader);
+  if (emit) {
+    const uint64_t pos = pack_count(old) + __popc(mask & ((1u << lane) - 1));
+    out[pos] = v;
+    out_dscan[pos] = pack_degsum(old) + dinc - dv;
+    atomicOr(out_bm + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// Sparse push straight from a frontier bitmap (the dense -> sparse
+// transition), with no id list or degree prefix built first: each warp
+// takes strided batches of up to 8 frontier words, packs the batch's
+// members onto the lanes 32 per round, and every lane walks its member's
+// list in lock-step with the warp (one step = one neighbour per lane, an
+// aggregated emission per step); lists longer than kPullSerial finish
+// warp-cooperatively, 32 neighbours per step.  Semantics as push_tile
+// (traversal.cpp:16-46: cond, claim, update, emit).  Callers guarantee
+// every member's degree is at most kBitmapPushMaxDeg (the dense level that
+// built the bitmap flags larger ones, and then the list path runs).  At
+// scale 24 this replaces the level-3 compaction (two passes over the
+// bitmap with a scattered degree lookup per member, a grid barrier and a
+// scan) and the per-tile searches over the 841K-member list.
+template <class G, class Op>
+__device__ GBG_PB_INLINE void push_bitmap(G g, const uint32_t* fbm, uint64_t nwords, Op op, uint32_t* out,
+                                            uint64_t* out_dscan, uint32_t* out_bm, unsigned long long* packed) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t per = (nwords + nwarps - 1) / nwarps;
+  const uint32_t B = static_cast<uint32_t>(per < kCwBatch ? (per ? per : 1) : kCwBatch);
+  for (uint64_t wb = gwarp * B; wb < nwords; wb += nwarps * B) {
+    const uint64_t wl = wb + lane;
+    const uint32_t fw = wl < wb + B && wl < nwords ? fbm[wl] : 0u;
+    const uint32_t pc = __popc(fw);
+    const uint32_t excl = warp_inclusive_scan(pc) - pc;
+    const uint32_t total = __shfl_sync(0xffffffffu, excl + pc, 31);
+    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+      const uint32_t t = r0 + lane;
+      const bool c = t < total;
+      uint32_t j = 0, ej = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < kCwBatch; ++k) {
+        const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
+        if (k < B && ek <= t) {
+          j = k;
+          ej = ek;
+        }
+      }
+      const uint32_t fwj = __shfl_sync(0xffffffffu, fw, j);
+      const uint32_t u = c ? static_cast<uint32_t>((wb + j) * 32 + __fns(fwj, 0, static_cast<int>(t - ej + 1))) : 0u;
+      uint64_t b = 0;
+      uint32_t d = 0;
+      if (c) g.seg(u, b, d);
+      const uint32_t ds = d < kPullSerial ? d : kPullSerial;
+      uint32_t steps = ds;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+      for (uint32_t k = 0; k < steps; ++k) {
+        uint32_t v = 0;
+        bool emit = false;
+        if (k < ds) {
+          v = g.at(b + k);
+          emit = op.cond(v) && op.claim(v) && op.update(u, v);
+        }
+        emit_warp(g, emit, v, out, out_dscan, out_bm, packed);
+      }
+      uint32_t hard = __ballot_sync(0xffffffffu, d > kPullSerial);
+      while (hard) {
+        const int l = __ffs(hard) - 1;
+        hard &= hard - 1;
+        const uint64_t bb = __shfl_sync(0xffffffffu, b, l);
+        const uint32_t dd = __shfl_sync(0xffffffffu, d, l);
+        const uint32_t uu = __shfl_sync(0xffffffffu, u, l);
+        for (uint32_t j0 = kPullSerial; j0 < dd; j0 += 32) {
+          const uint32_t jj = j0 + lane;
+          uint32_t v = 0;
+          bool emit = false;
+          if (jj < dd) {
+            v = g.at(bb + jj);
+            emit = op.cond(v) && op.claim(v) && op.update(uu, v);
+          }
+          emit_warp(g, emit, v, out, out_dscan, out_bm, packed);
+        }
+      }
+    }
+  }
 }
 
 }  // namespace gbg

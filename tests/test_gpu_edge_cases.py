@@ -190,6 +190,46 @@ def test_launch_per_step_paths_match_oracle(gbg, orc, tmp_path):
         assert np.array_equal(np.array(got[name][3], dtype=np.uint32), col), name
 
 
+def test_bfs_list_built_transitions_match_oracle(gbg, orc):
+    """GBG_BFS_BITMAP_PUSH=0 (fresh process): the persistent BFS builds the id
+    list at every dense -> sparse transition instead of pushing from the
+    bitmap; depths, direction trace and examined arcs still match the
+    oracle (R-MAT scale 16 and the bitmap-push transition graph)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from tests.test_gpu_parity import transition_graph
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n0, edges = transition_graph(1000)
+    tn, tpairs = undirected(n0, edges, orc)
+    code = (
+        "import sys, json; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_2405_11671_b200.graph as gbg\n"
+        "from oracle.bindings import RMAT_A, RMAT_B, RMAT_C\n"
+        "g = gbg.generate_rmat(16, 16 << 16, 1, RMAT_A, RMAT_B, RMAT_C)\n"
+        "t = gbg.CsrGraph.build(%d, np.array(json.loads(sys.stdin.read()), dtype=np.uint32))\n"
+        "out = {}\n"
+        "for name, h in (('rmat', g), ('transition', t)):\n"
+        "    r = gbg.bfs(h, 0)\n"
+        "    out[name] = [r.depth.tolist(), r.modes, r.examined]\n"
+        "print(json.dumps(out))\n" % (root, tn))
+    env = dict(os.environ, GBG_BFS_BITMAP_PUSH="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                         input=json.dumps(np.asarray(tpairs).tolist()))
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    n, pairs = orc.rmat(16, 16 << 16, 1)
+    for name, (nn, pp) in (("rmat", (n, pairs)), ("transition", (tn, tpairs))):
+        off, nbr = csr(nn, pp)
+        d, modes, _ = orc.bfs(nn, off, nbr, 0)
+        assert np.array_equal(np.array(got[name][0], dtype=np.int32), d), name
+        assert got[name][1] == modes, name
+        assert got[name][2] == orc.bfs_examined(nn, off, nbr, 0), name
+
+
 def test_concurrent_reads_from_threads(gbg, orc):
     """graph_container.hpp:33-35: read operations are safe from many threads.
     Several host threads run BFS / CC / degree queries on one handle (calls

@@ -220,6 +220,41 @@ def test_bfs_matches_oracle_seeded(gbg, ref, orc, kind):
         assert r.modes == modes and r.frontier_sizes == sizes
 
 
+def transition_graph(hub_degree):
+    """A BFS from 0 whose level 2 is dense and whose level 3 is a sparse push
+    from that level's bitmap holding one vertex of degree `hub_degree`:
+    0 - {1..1200}, 1 - H, H - (hub_degree - 1) leaves, and disjoint filler
+    edges that bring m to 40,000 arcs (threshold m/20 = 2000)."""
+    edges = [(0, a) for a in range(1, 1201)]
+    h = 1201
+    edges.append((1, h))
+    leaves = range(h + 1, h + hub_degree)
+    edges += [(h, x) for x in leaves]
+    nxt = h + hub_degree
+    fill = 20000 - len(edges)
+    edges += [(nxt + 2 * i, nxt + 2 * i + 1) for i in range(fill)]
+    return nxt + 2 * fill, edges
+
+
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
+@pytest.mark.parametrize("hub_degree", [40, 1000, 1024, 1025, 1500])
+def test_bfs_dense_to_sparse_transition(gbg, orc, kind, hub_degree):
+    """The dense -> sparse transition pushes straight from the frontier
+    bitmap when every member's degree is <= 1024 (lists above kPullSerial
+    finish warp-cooperatively) and builds the id list first otherwise; both
+    give the oracle's depths and direction trace."""
+    n0, edges = transition_graph(hub_degree)
+    n, pairs = undirected(n0, edges, orc)
+    off, nbr = csr(n, pairs)
+    g = gbg.CsrGraph.build(n, pairs) if kind == "csr" else gbg.BlockedGraph.build(n, pairs)
+    d, modes, sizes = orc.bfs(n, off, nbr, 0)
+    assert modes[:3] == [0, 1, 0] and sizes[2] == 1
+    r = gbg.bfs(g, 0)
+    assert np.array_equal(r.depth, d)
+    assert r.modes == modes and r.frontier_sizes == sizes
+    assert r.examined == orc.bfs_examined(n, off, nbr, 0)
+
+
 @pytest.mark.parametrize("S", [16, 20])
 def test_rmat_generator_and_bfs_cc_match_golden(gbg, S):
     gd = golden(S)
