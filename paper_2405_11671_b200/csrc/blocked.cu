@@ -140,9 +140,11 @@ __global__ void make_keys_k(const uint32_t* pairs, uint64_t count, uint64_t n, B
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
     const uint32_t s = pairs[2 * i], d = pairs[2 * i + 1];
-    if (s >= n || d >= n) *bad = 1;
-    // self-loops become the all-ones key, itself a self-loop, dropped below
-    keys[i] = s == d ? bk.loop_key() : bk.make(s, d);
+    const bool oor = s >= n || d >= n;
+    if (oor) *bad = 1;
+    // self-loops (and out-of-range arcs, which fail the call before any
+    // change) become the all-ones key, itself a self-loop, dropped below
+    keys[i] = s == d || oor ? bk.loop_key() : bk.make(s, d);
   }
 }
 
@@ -176,10 +178,13 @@ __global__ void contains_k(G g, const uint32_t* pairs, uint64_t count, uint8_t* 
 // presence of each prepared arc in the container (flag = changes the
 // container: absent for insert, present for delete) and its rank among the
 // source's current neighbours (the merge slot offset of an inserted arc)
-__global__ void apply_flags_k(const uint64_t* k, uint64_t U, BatchKeys bk, const uint64_t* start, const uint32_t* deg,
-                              const uint32_t* pool, int insert, uint32_t* flag, uint32_t* lb) {
+__global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t* U_dev, BatchKeys bk,
+                              const uint64_t* start, const uint32_t* deg, const uint32_t* pool, int insert,
+                              uint32_t* flag, uint32_t* lb) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < U; i += stride) {
+  const uint64_t U = *U_dev;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    if (i >= U) break;
     const uint64_t x = k[i];
     const uint32_t s = bk.src(x), d = bk.dst(x);
     const uint32_t* lst = pool + start[s];
@@ -192,12 +197,13 @@ __global__ void apply_flags_k(const uint64_t* k, uint64_t U, BatchKeys bk, const
 }
 struct ApplyOut {
   const uint32_t* flag;
+  const uint64_t* U;
   const uint64_t* k;
   const uint32_t* lb;
   uint64_t* out;
   uint32_t* out_lb;
   __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
-    if (flag[i]) {
+    if (i < *U && flag[i]) {
       out[pre] = k[i];
       out_lb[pre] = lb[i];
     }
@@ -208,17 +214,19 @@ struct ApplyOut {
 struct HeadIn {
   const uint64_t* k;
   BatchKeys bk;
+  const uint32_t* A;  // applied arcs (device count)
   __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
-    return i == 0 || bk.src(k[i - 1]) != bk.src(k[i]);
+    return i < *A && (i == 0 || bk.src(k[i - 1]) != bk.src(k[i]));
   }
 };
 struct HeadOut {
   const uint64_t* k;
   BatchKeys bk;
+  const uint32_t* A;
   uint32_t* gstart;  // first applied arc of group
   uint32_t* gsrc;
   __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
-    if (HeadIn{k, bk}(i)) {
+    if (HeadIn{k, bk, A}(i)) {
       gstart[pre] = static_cast<uint32_t>(i);
       gsrc[pre] = bk.src(k[i]);
     }
@@ -226,11 +234,14 @@ struct HeadOut {
 };
 
 // per group: new degree / capacity, and whether it needs a fresh allocation
-__global__ void group_plan_k(uint32_t ng, uint32_t A, const uint32_t* gstart, const uint32_t* gsrc,
-                             const uint32_t* deg, const uint32_t* cap, int insert, uint32_t* gcnt, uint32_t* gnewdeg,
-                             uint32_t* gnewcap, uint64_t* galloc, int* underflow) {
+__global__ void group_plan_k(uint64_t count, const uint32_t* ng_dev, const uint32_t* A_dev, uint32_t* gstart,
+                             const uint32_t* gsrc, const uint32_t* deg, const uint32_t* cap, int insert,
+                             uint32_t* gcnt, uint32_t* gnewdeg, uint32_t* gnewcap, uint64_t* galloc, int* underflow) {
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += stride) {
+  const uint32_t ng = *ng_dev, A = *A_dev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) gstart[ng] = A;  // closes the last group (read below only for gi + 1 < ng)
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < count; gi += stride) {
+    if (gi >= ng) break;
     const uint32_t c = (gi + 1 < ng ? gstart[gi + 1] : A) - gstart[gi];
     const uint32_t s = gsrc[gi];
     const uint32_t d = deg[s];
@@ -253,7 +264,8 @@ __global__ void group_plan_k(uint32_t ng, uint32_t A, const uint32_t* gstart, co
 struct OldDegIn {
   const uint32_t* gsrc;
   const uint32_t* deg;
-  __device__ __forceinline__ uint64_t operator()(uint64_t gi) const { return deg[gsrc[gi]]; }
+  const uint32_t* ng;
+  __device__ __forceinline__ uint64_t operator()(uint64_t gi) const { return gi < *ng ? deg[gsrc[gi]] : 0; }
 };
 
 // Staging, merge and set difference run on the balanced segmented
@@ -336,28 +348,53 @@ __global__ void refresh_caps_k(uint64_t n, const uint32_t* deg, uint32_t* cap) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) cap[v] = cap_for(deg[v]);
 }
 
-// prepare(GlobalSort) on the device; returns the unique, self-loop-free
-// keys (sorted) and their count.
-// *free_out receives the other key buffer (free scratch afterwards).
-uint64_t prepare_device(gbg_graph* g, const uint32_t* pairs, uint64_t count, BatchKeys bk, uint64_t** ukeys_out,
-                        uint64_t** free_out) {
-  uint64_t* keys = g->ws.get<uint64_t>("upd.keys", count);
-  uint64_t* sorted = g->ws.get<uint64_t>("upd.sorted", count);
-  int* bad = g->ws.get<int>("upd.bad", 1);
-  GBG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
-  GBG_LAUNCH(g, make_keys_k, grid_for(count, 256), 256, 0, pairs, count, g->n, bk, keys, bad);
-  int hb = 0;
-  read_scalars(g, bad, sizeof(hb), &hb);
-  if (hb) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
-  uint64_t U = 0;
-  PhaseTrace tr(g->stream, "prepare");
-  uint64_t* uk = sort_unique_keys(g, keys, sorted, count, bk, &U, "upd");
-  tr.mark("sort+unique");
-  *ukeys_out = uk;
-  *free_out = uk == keys ? sorted : keys;
-  return U;
+// Scan inputs / outputs over a prefix whose length lives in device memory
+// (the scans are sized by the raw arc count, an upper bound).
+template <class T, class N>
+struct BoundedIn {
+  const T* a;
+  const N* n;
+  __device__ __forceinline__ T operator()(uint64_t i) const { return i < *n ? a[i] : T(0); }
+};
+template <class T, class N>
+struct BoundedOut {  // writes [0, n]: the exclusive prefix at n is the total (scan count + 1 elements)
+  T* a;
+  const N* n;
+  __device__ __forceinline__ void operator()(uint64_t i, T v) const {
+    if (i <= *n) a[i] = v;
+  }
+};
+
+// Device-side scalars of one batch, read back to the host once.
+struct UpdScalars {
+  uint64_t U;     // unique, self-loop-free arcs (prepare)
+  uint64_t need;  // pool ids the grown lists allocate
+  uint64_t otot;  // old list sizes of the touched sources (staging)
+  uint32_t A;     // applied arcs
+  uint32_t ng;    // touched sources
+  int bad;        // an endpoint >= n
+  int under;      // metadata underflow
+};
+
+// Grow the pool when the batch's allocations do not fit (rare): the live
+// lists are compacted into a larger pool and the allocation plan redone.
+static void plan_allocations(gbg_graph* g, uint64_t count, uint32_t* gstart, const uint32_t* gsrc, bool insert,
+                             UpdScalars* sc, uint32_t* gcnt, uint32_t* gnewdeg, uint32_t* gnewcap, uint64_t* galloc,
+                             uint64_t* gascan) {
+  GBG_LAUNCH(g, group_plan_k, grid_for(count, 256, g->sm_count * 16), 256, 0, count, &sc->ng, &sc->A, gstart, gsrc,
+             g->bdeg, g->bcap, insert ? 1 : 0, gcnt, gnewdeg, gnewcap, galloc, &sc->under);
+  device_scan<uint64_t>(g, BoundedIn<uint64_t, uint32_t>{galloc, &sc->ng},
+                        BoundedOut<uint64_t, uint32_t>{gascan, &sc->ng}, count + 1, &sc->need, "upd.alloc");
 }
 
+// The whole batch up to the staging step runs without a host round trip:
+// every stage is sized by the raw arc count (an upper bound of U, A and
+// the group count) and reads the actual counts from device memory; one
+// readback then brings U, A, the group count, the allocation need, the
+// staging size and the error flags (out-of-range ids were turned into
+// dropped keys, so nothing before the readback can fault), and errors are
+// raised before the container is touched.  A 10^4-edge batch went from
+// eight host synchronisations to one.
 uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bool insert) {
   if (g->kind != GBG_KIND_BLOCKED)
     fail(GBG_ERR_UNSUPPORTED, insert ? "container is static: batch insert not supported"
@@ -366,57 +403,59 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   if (count > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "batch too large (max 2^32-1 arcs)");
   const BatchKeys bk{key_bits(g->n)};
   PhaseTrace tr(g->stream, insert ? "insert_batch" : "delete_batch");
-  uint64_t* ukeys = nullptr;
-  uint64_t* akeys = nullptr;  // the free key buffer receives the applied arcs
-  const uint32_t U = static_cast<uint32_t>(prepare_device(g, pairs_dev, count, bk, &ukeys, &akeys));
+  UpdScalars* sc = g->ws.get<UpdScalars>("upd.sc", 1);
+  GBG_CUDA(cudaMemsetAsync(sc, 0, sizeof(UpdScalars), g->stream));
+  // prepare(GlobalSort): keys, radix sort, unique (batch.cpp:34-42)
+  uint64_t* keys = g->ws.get<uint64_t>("upd.keys", count);
+  uint64_t* sorted = g->ws.get<uint64_t>("upd.sorted", count);
+  GBG_LAUNCH(g, make_keys_k, grid_for(count, 256), 256, 0, pairs_dev, count, g->n, bk, keys, &sc->bad);
+  uint64_t* srt = radix_sort_u64(g, keys, sorted, count, 2 * bk.L, "upd");
+  uint64_t* ukeys = srt == keys ? sorted : keys;
+  device_scan<uint64_t>(g, UniqueIn{srt, bk}, UniqueOut{srt, bk, ukeys}, count, &sc->U, "upd.uniq");
+  uint64_t* akeys = srt;  // free again: receives the applied arcs
   tr.mark("prepare");
-  if (U == 0) return 0;
-  uint32_t* cnt = g->ws.get<uint32_t>("upd.cnt", 4);
-  uint32_t* flag = g->ws.get<uint32_t>("upd.flag", U);
-  uint32_t* lb = g->ws.get<uint32_t>("upd.lb", U);
-  uint32_t* alb = g->ws.get<uint32_t>("upd.alb", U);
-  GBG_LAUNCH(g, apply_flags_k, grid_for(U, 256, g->sm_count * 16), 256, 0, ukeys, U, bk, g->bstart, g->bdeg, g->pool,
-             insert ? 1 : 0, flag, lb);
-  device_scan<uint32_t>(g, ArrayIn<uint32_t>{flag}, ApplyOut{flag, ukeys, lb, akeys, alb}, U, cnt + 1, "upd.apply");
-  uint32_t A = 0;
-  read_scalars(g, cnt + 1, sizeof(A), &A);
-  if (A == 0) return 0;
-  uint32_t* gstart = g->ws.get<uint32_t>("upd.gstart", A + 1);
-  uint32_t* gsrc = g->ws.get<uint32_t>("upd.gsrc", A);
-  device_scan<uint32_t>(g, HeadIn{akeys, bk}, HeadOut{akeys, bk, gstart, gsrc}, A, cnt + 2, "upd.heads");
-  uint32_t ng = 0;
-  read_scalars(g, cnt + 2, sizeof(ng), &ng);
-  GBG_CUDA(cudaMemcpyAsync(gstart + ng, &A, sizeof(A), cudaMemcpyHostToDevice, g->stream));  // gstart[ng] = A
+  // presence of each unique arc -> the applied arcs and their merge slots
+  uint32_t* flag = g->ws.get<uint32_t>("upd.flag", count);
+  uint32_t* lb = g->ws.get<uint32_t>("upd.lb", count);
+  uint32_t* alb = g->ws.get<uint32_t>("upd.alb", count);
+  GBG_LAUNCH(g, apply_flags_k, grid_for(count, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk, g->bstart,
+             g->bdeg, g->pool, insert ? 1 : 0, flag, lb);
+  device_scan<uint32_t>(g, BoundedIn<uint32_t, uint64_t>{flag, &sc->U}, ApplyOut{flag, &sc->U, ukeys, lb, akeys, alb},
+                        count, &sc->A, "upd.apply");
+  // groups by source
+  uint32_t* gstart = g->ws.get<uint32_t>("upd.gstart", count + 1);
+  uint32_t* gsrc = g->ws.get<uint32_t>("upd.gsrc", count);
+  device_scan<uint32_t>(g, HeadIn{akeys, bk, &sc->A}, HeadOut{akeys, bk, &sc->A, gstart, gsrc}, count, &sc->ng,
+                        "upd.heads");
   tr.mark("presence+groups");
-  uint32_t* gcnt = g->ws.get<uint32_t>("upd.gcnt", ng);
-  uint32_t* gnewdeg = g->ws.get<uint32_t>("upd.gnewdeg", ng);
-  uint32_t* gnewcap = g->ws.get<uint32_t>("upd.gnewcap", ng);
-  uint64_t* galloc = g->ws.get<uint64_t>("upd.galloc", ng);
-  uint64_t* gascan = g->ws.get<uint64_t>("upd.gascan", ng + 1);
-  int* under = g->ws.get<int>("upd.under", 1);
-  for (int attempt = 0;; ++attempt) {
-    GBG_CUDA(cudaMemsetAsync(under, 0, sizeof(int), g->stream));
-    GBG_LAUNCH(g, group_plan_k, grid_for(ng, 256), 256, 0, ng, A, gstart, gsrc, g->bdeg, g->bcap, insert ? 1 : 0,
-               gcnt, gnewdeg, gnewcap, galloc, under);
-    device_scan<uint64_t>(g, ArrayIn<uint64_t>{galloc}, ArrayOut<uint64_t>{gascan}, ng, gascan + ng, "upd.alloc");
-    uint64_t need = 0;
-    read_scalars(g, gascan + ng, sizeof(need), &need);
-    int hu = 0;
-    read_scalars(g, under, sizeof(hu), &hu);
-    if (hu) fail(GBG_ERR_LOGIC, "metadata underflow: tracker and container diverged");
-    if (g->pool_top + need <= g->pool_cap) break;
-    if (attempt > 0) fail(GBG_ERR_OOM, "blocked pool exhausted after compaction");
-    // compact into a larger pool (caps refreshed to the current degrees)
+  uint32_t* gcnt = g->ws.get<uint32_t>("upd.gcnt", count);
+  uint32_t* gnewdeg = g->ws.get<uint32_t>("upd.gnewdeg", count);
+  uint32_t* gnewcap = g->ws.get<uint32_t>("upd.gnewcap", count);
+  uint64_t* galloc = g->ws.get<uint64_t>("upd.galloc", count);
+  uint64_t* gascan = g->ws.get<uint64_t>("upd.gascan", count + 1);
+  plan_allocations(g, count, gstart, gsrc, insert, sc, gcnt, gnewdeg, gnewcap, galloc, gascan);
+  uint64_t* oscan = g->ws.get<uint64_t>("upd.oscan", count + 1);
+  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng}, BoundedOut<uint64_t, uint32_t>{oscan, &sc->ng},
+                        count + 1, &sc->otot, "upd.oscan");
+  UpdScalars h;
+  read_scalars(g, sc, sizeof(h), &h);
+  tr.mark("plan");
+  if (h.bad) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
+  if (h.U == 0 || h.A == 0) return 0;
+  if (h.under) fail(GBG_ERR_LOGIC, "metadata underflow: tracker and container diverged");
+  const uint32_t A = h.A, ng = h.ng;
+  if (g->pool_top + h.need > g->pool_cap) {
+    // compact into a larger pool (caps refreshed to the current degrees),
+    // then plan again against the new capacities
     GBG_LAUNCH(g, refresh_caps_k, grid_for(g->n, 256), 256, 0, g->n, g->bdeg, g->bcap);
-    blocked_relayout(g, g->bstart, g->pool, 2 * need, true);
+    blocked_relayout(g, g->bstart, g->pool, 2 * h.need, true);
+    plan_allocations(g, count, gstart, gsrc, insert, sc, gcnt, gnewdeg, gnewcap, galloc, gascan);
+    read_scalars(g, &sc->need, sizeof(h.need), &h.need);
+    if (g->pool_top + h.need > g->pool_cap) fail(GBG_ERR_OOM, "blocked pool exhausted after compaction");
   }
   // stage the touched old lists
-  uint64_t* oscan = g->ws.get<uint64_t>("upd.oscan", ng + 1);
-  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg}, ArrayOut<uint64_t>{oscan}, ng, oscan + ng, "upd.oscan");
-  uint64_t otot = 0;
-  read_scalars(g, oscan + ng, sizeof(otot), &otot);
+  const uint64_t otot = h.otot;
   uint32_t* staged = g->ws.get<uint32_t>("upd.staged", otot);
-  tr.mark("plan");
   expand(g, oscan, ng, otot, StageOp{gsrc, g->bstart, g->pool, staged});
   tr.mark("stage");
   // destinations
@@ -427,9 +466,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,
              g->bcap);
   tr.mark("merge");
-  uint64_t need = 0;
-  read_scalars(g, gascan + ng, sizeof(need), &need);
-  g->pool_top += need;
+  g->pool_top += h.need;
   if (insert) {
     g->m += A;
   } else {
