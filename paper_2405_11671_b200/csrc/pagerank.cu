@@ -233,6 +233,52 @@ void layout_relabel(gbg_graph* g, G view, const uint64_t* voff, PrLayout* L, uin
   for_each_edge_range(g, view, voff, e0, e1, RelabelCheckedOp{RelabelOp{voff, L->pos, L->off, L->nbr}, g->n});
 }
 
+// Heavy rows (> 4096 edges: the hubs, first in the degree order) get their
+// relabelled lists sorted ascending.  A warp of the chunked heavy-row path
+// reads 32 consecutive entries per gather, and in a sorted hub list the
+// many neighbours inside the dense hot region share 128-byte lines, so the
+// gather instruction needs fewer L1 wavefronts (scale 24: 48.2 -> 46.4 ms
+// for 20 iterations; sorting the other rows as well gains nothing more,
+// sorting only within 4096-entry chunks half as much).  One stable radix
+// sort of (row, id) keys over the heavy rows' arcs: +10.8 ms of layout
+// build at scale 24, paid once per graph version by gbg_pagerank_prepare /
+// the first PageRank call.  The pipelined create (gbg_csr_create_ex with
+// GBG_CREATE_PAGERANK_LAYOUT) skips it: hub rows complete only when their
+// last chunk lands, anywhere in the upload, so the sort would be exposed
+// (+10-18 ms) for a 1.8 ms saving on a 20-iteration call.
+struct HeavyKeyOp {
+  uint64_t* keys;
+  int idb;
+  __device__ __forceinline__ void operator()(uint32_t u, uint32_t v, uint64_t e) const {
+    keys[e] = (static_cast<uint64_t>(u) << idb) | v;
+  }
+};
+__global__ void heavy_unkey_k(const uint64_t* keys, uint64_t count, int idb, uint32_t* nbr) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count; e += stride)
+    nbr[e] = static_cast<uint32_t>(keys[e] & ((uint64_t{1} << idb) - 1));
+}
+void layout_sort_heavy(gbg_graph* g, PrLayout* L) {
+  const uint32_t nheavy = L->row_begin[1];
+  if (!nheavy) return;
+  uint64_t H = 0;
+  read_scalars(g, L->off + nheavy, sizeof(H), &H);
+  if (!H) return;
+  int idb = 1, rb = 1;
+  while ((uint64_t{1} << idb) < L->n) ++idb;
+  while ((uint64_t{1} << rb) < nheavy) ++rb;
+  uint64_t* keys = g->ws.get<uint64_t>("prl.hkeys", H);
+  uint64_t* scr = g->ws.get<uint64_t>("prl.hscr", H);
+  CsrView lv{L->n, L->off, L->nbr};
+  for_each_edge_range(g, lv, L->off, 0, H, HeavyKeyOp{keys, idb});
+  const uint64_t* sorted = radix_sort_u64(g, keys, scr, H, rb + idb, "prl.hsort");
+  GBG_LAUNCH(g, heavy_unkey_k, grid_for(H, 256), 256, 0, sorted, H, idb, L->nbr);
+  g->ws.release("prl.hkeys");
+  g->ws.release("prl.hscr");
+  g->ws.release("prl.hsort.hist");
+  g->ws.release("prl.hsort.lb");
+}
+
 template <class G>
 PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   cudaEvent_t e0, e1;
@@ -241,6 +287,7 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
   GBG_CUDA(cudaEventRecord(e0, g->stream));
   PrLayout* L = layout_rows(g, view);
   layout_relabel(g, view, voff, L, 0, g->m);
+  layout_sort_heavy(g, L);
   GBG_CUDA(cudaEventRecord(e1, g->stream));
   GBG_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
