@@ -342,9 +342,21 @@ __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32
 
 // Sum of fmax(X[nbr[e]], 0) over e = b + t, b + t + T, ... (< b + d), with
 // all K id loads issued before the K gathers.
+// At most 8 id loads, then 8 gathers, in flight per thread: longer unrolls
+// (K = 16 / 32 in the class table) run as sequential batches of 8.  The
+// 16-wide form spilled the ids to local memory at the 32-register budget,
+// and every spilled line is an L1->L2 request on the path that limits this
+// kernel (l1tex2xbar request cycles ~70% of peak): s24 46.4 -> 44.8 ms.
+#ifndef GBG_PR_KMAX
+#define GBG_PR_KMAX 8
+#endif
 template <int K>
 __device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint64_t d, uint32_t t, uint32_t T,
                                              uint64_t pf, uint64_t pl) {
+  if constexpr (K > GBG_PR_KMAX) {
+    const double lo = gather_sum<GBG_PR_KMAX>(a, b, d, t, T, pf, pl);
+    return lo + gather_sum<K - GBG_PR_KMAX>(a, b, d, t + GBG_PR_KMAX * T, T, pf, pl);
+  }
   uint32_t ids[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
