@@ -301,6 +301,7 @@ PrLayout* build_layout(gbg_graph* g, G view, const uint64_t* voff) {
 // ---------------------------------------------------------------- iteration
 struct PrScalars {
   double dangling[2];  // ping-pong: iteration i reads [i&1], writes [(i+1)&1]
+  double p_zero;       // rank of every zero-degree row after the last executed iteration
   double err;          // L1 step difference of the last executed iteration
   int done;            // set once err < tolerance (algorithms.cpp:552)
   int iterations;      // iterations executed
@@ -321,23 +322,18 @@ struct PrArgs {
   uint32_t row_begin[kClasses + 1];
   uint64_t unit_begin[kClasses + 1];
   double damping, nd, tol;
+  double n_zero;  // zero-degree rows (the last class)
   int iter;
 };
 
-// Finalize row r (algorithms.cpp:544-550 for one vertex) and emit the next
-// iteration's contrib form.
+// Finalize row r (d > 0; algorithms.cpp:544-550 for one vertex) and emit
+// the next iteration's contrib form.
 __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32_t r, uint64_t d, double sum,
-                                            double& err, double& dang) {
+                                            double& err) {
   const double next = base + a.damping * sum;
   const double xo = __ldcs(a.x_old + r);
-  const double pold = d ? xo * static_cast<double>(d) : -xo;
-  err += fabs(next - pold);
-  if (d) {
-    a.x_new[r] = next / static_cast<double>(d);
-  } else {
-    a.x_new[r] = -next;
-    dang += next;
-  }
+  err += fabs(next - xo * static_cast<double>(d));
+  a.x_new[r] = next / static_cast<double>(d);
 }
 
 // Sum of fmax(X[nbr[e]], 0) over e = b + t, b + t + T, ... (< b + d), with
@@ -351,22 +347,23 @@ __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32
 #define GBG_PR_KMAX 8
 #endif
 template <int K>
-__device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint64_t d, uint32_t t, uint32_t T,
+__device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint32_t d, uint32_t t, uint32_t T,
                                              uint64_t pf, uint64_t pl) {
   if constexpr (K > GBG_PR_KMAX) {
     const double lo = gather_sum<GBG_PR_KMAX>(a, b, d, t, T, pf, pl);
     return lo + gather_sum<K - GBG_PR_KMAX>(a, b, d, t + GBG_PR_KMAX * T, T, pf, pl);
   }
+  const uint32_t* nb = a.nbr + b;
   uint32_t ids[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    const uint64_t k = t + static_cast<uint64_t>(j) * T;
-    ids[j] = k < d ? ld_stream_u32(a.nbr + b + k, pf) : 0u;
+    const uint32_t k = t + j * T;
+    ids[j] = k < d ? ld_stream_u32(nb + k, pf) : 0u;
   }
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    const uint64_t k = t + static_cast<uint64_t>(j) * T;
+    const uint32_t k = t + j * T;
     double x = 0.0;
     if (k < d) x = ids[j] < kL1Hot ? ld_hot_f64(a.x_old + ids[j], pl) : ld_cold_f64(a.x_old + ids[j], pl);
     acc += fmax(x, 0.0);
@@ -383,10 +380,15 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   const double dcur = a.sc->dangling[a.iter & 1];
   const double base = (1.0 - a.damping) / a.nd + a.damping * dcur / a.nd;
-  double err = 0.0, dang = 0.0;
-  const uint64_t total = a.unit_begin[kClasses];
+  double err = 0.0;
+  // Zero-degree rows (the last class; 7.9M of 16.8M at scale 24) are not
+  // visited: none is anyone's neighbour, and each one's next rank is exactly
+  // `base` (base + damping * 0), so their dangling mass is n_zero * base and
+  // their L1 step is n_zero * |base - previous base|, folded in below, and
+  // the output maps them to the last base (pr_to_p_k).
+  const uint32_t total = static_cast<uint32_t>(a.unit_begin[kClasses - 1]);
 
-  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+  for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
     int c = 0;
 #pragma unroll
     for (int k = 1; k < kClasses; ++k)
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
       const uint64_t rb = __ldg(a.off + r), re = __ldg(a.off + r + 1);
       const uint32_t nch = static_cast<uint32_t>((re - rb + kChunk - 1) / kChunk);
       const uint64_t eb = rb + (w - c0) * kChunk;
-      const uint64_t len = eb + kChunk < re ? kChunk : re - eb;
+      const uint32_t len = static_cast<uint32_t>(eb + kChunk < re ? kChunk : re - eb);
       const double s = block_sum(gather_sum<kChunk / kPrThreads>(a, eb, len, threadIdx.x, kPrThreads, pf, pl), s_red);
       if (threadIdx.x == 0) {
         a.heavy_partial[w] = s;
@@ -410,20 +412,21 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
         __threadfence();
         double tot = 0.0;
         for (uint32_t k = 0; k < nch; ++k) tot += __ldcg(a.heavy_partial + c0 + k);
-        pr_finalize(a, base, r, re - rb, tot, err, dang);
+        pr_finalize(a, base, r, re - rb, tot, err);
         a.heavy_counter[r] = 0;
       }
       __syncthreads();
     } else if (class_threads(c) == kPrThreads) {
       // ---- one CTA per row
       const uint32_t r = a.row_begin[c] + static_cast<uint32_t>(w - a.unit_begin[c]);
-      const uint64_t rb = __ldg(a.off + r), d = __ldg(a.off + r + 1) - rb;
+      const uint64_t rb = __ldg(a.off + r);
+      const uint32_t d = static_cast<uint32_t>(__ldg(a.off + r + 1) - rb);
       double p;
       if (class_k(c) == 16) p = gather_sum<16>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
       else if (class_k(c) == 8) p = gather_sum<8>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
       else p = gather_sum<4>(a, rb, d, threadIdx.x, kPrThreads, pf, pl);
       const double s = block_sum(p, s_red);
-      if (threadIdx.x == 0) pr_finalize(a, base, r, d, s, err, dang);
+      if (threadIdx.x == 0) pr_finalize(a, base, r, d, s, err);
     } else {
       // ---- a fixed group of lanes per row, rows of the unit consecutive
       const uint32_t lanes = class_threads(c);
@@ -433,13 +436,13 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
       const uint32_t r = static_cast<uint32_t>(r64);
       const uint32_t l = threadIdx.x & (lanes - 1);
       double acc = 0.0;
-      uint64_t d = 0;
+      uint32_t d = 0;
       if (valid) {
         const uint64_t rb = ld_stream_u64(a.off + r, pf);
-        d = ld_stream_u64(a.off + r + 1, pf) - rb;
+        d = static_cast<uint32_t>(ld_stream_u64(a.off + r + 1, pf) - rb);
         switch (class_k(c)) {
           case 32:  // warp per row, 512 edges per pass (no block barrier)
-            for (uint64_t o = 0; o < d; o += 16 * 32) acc += gather_sum<16>(a, rb + o, d - o, l, 32, pf, pl);
+            for (uint32_t o = 0; o < d; o += 16 * 32) acc += gather_sum<16>(a, rb + o, d - o, l, 32, pf, pl);
             break;
           case 16: acc = gather_sum<16>(a, rb, d, l, lanes, pf, pl); break;
           case 8: acc = gather_sum<8>(a, rb, d, l, lanes, pf, pl); break;
@@ -450,31 +453,27 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
         }
       }
       for (uint32_t o = lanes >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, lanes);
-      if (valid && l == 0) pr_finalize(a, base, r, d, acc, err, dang);
+      if (valid && l == 0) pr_finalize(a, base, r, d, acc, err);
     }
   }
 
   // ---- per-CTA partials, last CTA folds them in order
   const double be = block_sum(err, s_red);
-  const double bd = block_sum(dang, s_red);
   if (threadIdx.x == 0) {
-    a.blk[2 * blockIdx.x] = be;
-    a.blk[2 * blockIdx.x + 1] = bd;
+    a.blk[blockIdx.x] = be;
     __threadfence();
     s_flag = atomicAdd(a.done_counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (s_flag) {
     __threadfence();
-    double e = 0.0, dg = 0.0;
-    for (uint64_t k = threadIdx.x; k < gridDim.x; k += kPrThreads) {
-      e += __ldcg(a.blk + 2 * k);
-      dg += __ldcg(a.blk + 2 * k + 1);
-    }
+    double e = 0.0;
+    for (uint64_t k = threadIdx.x; k < gridDim.x; k += kPrThreads) e += __ldcg(a.blk + k);
     e = block_sum(e, s_red);
-    dg = block_sum(dg, s_red);
     if (threadIdx.x == 0) {
-      a.sc->dangling[(a.iter + 1) & 1] = dg;
+      e += a.n_zero * fabs(base - a.sc->p_zero);
+      a.sc->dangling[(a.iter + 1) & 1] = a.n_zero * base;
+      a.sc->p_zero = base;
       a.sc->err = e;
       a.sc->iterations = a.iter + 1;
       if (e < a.tol) a.sc->done = 1;
@@ -483,12 +482,17 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
   }
 }
 
-__global__ void pr_init_k(const uint64_t* off, uint64_t n, double* x) {
+// X0 = contrib form of p0; zero-degree rows (never written by the
+// iterations) hold a non-positive value in both buffers, so a gather of
+// one (an arc into a vertex without out-arcs, after asymmetric updates)
+// contributes fmax(x, 0) = 0 as the reference's contrib[u] = 0 does
+__global__ void pr_init_k(const uint64_t* off, uint64_t n, double* x, double* x1) {
   const double p0 = 1.0 / static_cast<double>(n);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
     const uint64_t d = off[r + 1] - off[r];
     x[r] = d ? p0 / static_cast<double>(d) : -p0;
+    if (!d) x1[r] = -p0;
   }
 }
 
@@ -498,20 +502,23 @@ struct DanglingIn {
   __device__ __forceinline__ double operator()(uint64_t r) const { return off[r + 1] - off[r] ? 0.0 : p0; }
 };
 
-// p[old id] from the contrib form of the renumbered vector
-__global__ void pr_to_p_k(const uint64_t* off, const uint32_t* pos, uint64_t n, const double* x, double* p) {
+// p[old id] from the contrib form of the renumbered vector (zero-degree
+// rows: the rank of the last executed iteration, sc->p_zero)
+__global__ void pr_to_p_k(const uint64_t* off, const uint32_t* pos, uint64_t n, const double* x,
+                          const PrScalars* sc, double* p) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const double pz = sc->p_zero;
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
     const uint32_t r = pos[v];
     const uint64_t d = off[r + 1] - off[r];
-    const double xr = x[r];
-    p[v] = d ? xr * static_cast<double>(d) : -xr;
+    p[v] = d ? x[r] * static_cast<double>(d) : pz;
   }
 }
 
-__global__ void pr_scalars_init_k(PrScalars* sc, const double* dangling0) {
+__global__ void pr_scalars_init_k(PrScalars* sc, const double* dangling0, double p0) {
   sc->dangling[0] = *dangling0;
   sc->dangling[1] = 0.0;
+  sc->p_zero = p0;
   sc->err = 0.0;
   sc->done = 0;
   sc->iterations = 0;
@@ -526,7 +533,7 @@ PrLayout* pr_layout(gbg_graph* g) {
     int per_sm = 1;
     GBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pr_iter_k, kPrThreads, 0));
     g->pr->grid = static_cast<uint32_t>(std::max(per_sm, 1) * g->sm_count);
-    g->pr->blk = dalloc<double>(2 * g->pr->grid);
+    g->pr->blk = dalloc<double>(g->pr->grid);
   }
   return g->pr;
 }
@@ -550,9 +557,9 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
   double* d0 = g->ws.get<double>("pr.d0", 1);
   PrScalars* sc = g->ws.get<PrScalars>("pr.sc", 1);
   const double p0 = 1.0 / static_cast<double>(n);
-  GBG_LAUNCH(g, pr_init_k, grid_for(n, 256), 256, 0, L->off, n, X0);
+  GBG_LAUNCH(g, pr_init_k, grid_for(n, 256), 256, 0, L->off, n, X0, X1);
   device_scan<double>(g, DanglingIn{L->off, p0}, NullOut{}, n, d0, "pr.dang");
-  GBG_LAUNCH(g, pr_scalars_init_k, 1, 1, 0, sc, d0);
+  GBG_LAUNCH(g, pr_scalars_init_k, 1, 1, 0, sc, d0, p0);
   double* X[2] = {X0, X1};
   for (uint64_t it = 0; it < max_iters; ++it) {
     PrArgs a;
@@ -573,6 +580,7 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
     a.nd = static_cast<double>(n);
     a.tol = tol;
     a.iter = static_cast<int>(it);
+    a.n_zero = static_cast<double>(n - L->row_begin[kClasses - 1]);
     GBG_LAUNCH(g, pr_iter_k, L->grid, kPrThreads, 0, a);
   }
   PrScalars hs;
@@ -581,7 +589,7 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
   std::memcpy(&hs, g->hscalar, sizeof(PrScalars));
   const uint64_t done = static_cast<uint64_t>(hs.iterations);
   // p lives in the X buffer written by the last executed iteration
-  GBG_LAUNCH(g, pr_to_p_k, grid_for(n, 256), 256, 0, L->off, L->pos, n, X[done & 1], p_dev);
+  GBG_LAUNCH(g, pr_to_p_k, grid_for(n, 256), 256, 0, L->off, L->pos, n, X[done & 1], sc, p_dev);
   return done;
 }
 

@@ -340,6 +340,23 @@ def test_pagerank_hub_rows(gbg, orc):
     assert rel_l1(got, want) <= PR_TOL
 
 
+def test_pagerank_asymmetric_arcs(gbg, orc):
+    """Directed arc sets: vertices with in-arcs but no out-arcs are dangling
+    (contrib 0, mass redistributed) yet gathered by their in-neighbours, on
+    both containers, with early stopping and with 20 fixed iterations."""
+    rng = np.random.default_rng(5)
+    for trial in range(8):
+        n = 200 + 150 * trial
+        raw = rng.integers(0, n, size=(3 * n, 2)).astype(np.uint32)
+        raw = raw[raw[:, 0] % 3 != 0]  # a third of the vertices keep no out-arcs
+        pairs = orc.prepare_global(raw)
+        off, nbr = csr(n, pairs)
+        for g in (gbg.CsrGraph.build(n, pairs), gbg.BlockedGraph.build(n, pairs)):
+            for tol in (1e-4, TINY):
+                want = orc.pagerank(n, off, nbr, 0.85, 20, tol)
+                assert rel_l1(gbg.pagerank(g, 0.85, 20, tol), want) <= PR_TOL, (trial, tol)
+
+
 # ---------------------------------------------------------------- CC / TC
 @pytest.mark.parametrize("kind", ["csr", "blocked"])
 def test_cc_matches_oracle(gbg, ref, orc, kind):
