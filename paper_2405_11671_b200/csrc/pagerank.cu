@@ -44,7 +44,10 @@ constexpr int kPrThreads = 256;
 constexpr uint32_t kChunk = 4096;  // edges per heavy-row chunk (16 per thread)
 // Gathers of the kL1Hot highest-degree vertices (128 KiB of contribs, ~28%
 // of all gathers at scale 24) may stay in L1; the rest bypass it.
-constexpr uint32_t kL1Hot = 16384;
+#ifndef GBG_PR_L1HOT
+#define GBG_PR_L1HOT 16384
+#endif
+constexpr uint32_t kL1Hot = GBG_PR_L1HOT;
 // Degree classes over the degree-descending rows: class c gives each row
 // T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
 // at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
