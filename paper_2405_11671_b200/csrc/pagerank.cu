@@ -54,15 +54,19 @@ constexpr uint32_t kL1Hot = GBG_PR_L1HOT;
 // 4096) splits rows into kChunk-edge chunks across CTAs; classes 1-2 (1025
 // to 4096) take a CTA per row; class 3 (513 to 1024) a warp per row in two
 // 512-edge passes (no block barrier: better at scale 24, while the CTA form
-// stays better for the longer rows, which dominate at scale 20); the last
-// class is the isolated rows (finalize only).
+// stays better for the longer rows, which dominate at scale 20); below 513
+// edges a row gets 16 / 8 / 4 / 2 / 1 lanes walking 16-32 edges each in
+// batches of 8 (fewer lanes per row, more rows per warp: scale 24 42.3 ->
+// 38.8 ms against the former 32 / 16 lanes x 4-16 edges, see
+// profiles/r01_pr_class_table.md); the last class is the isolated rows
+// (resolved analytically, not visited).
 constexpr int kClasses = 15;
 __host__ __device__ constexpr uint32_t class_threads(int c) {
-  constexpr uint32_t t[kClasses] = {256, 256, 256, 32, 32, 32, 32, 16, 8, 4, 2, 1, 1, 1, 1};
+  constexpr uint32_t t[kClasses] = {256, 256, 256, 32, 16, 8, 8, 4, 2, 1, 1, 1, 1, 1, 1};
   return t[c];
 }
 __host__ __device__ constexpr uint32_t class_k(int c) {
-  constexpr uint32_t k[kClasses] = {16, 16, 8, 32, 16, 8, 4, 4, 4, 4, 4, 4, 2, 1, 0};
+  constexpr uint32_t k[kClasses] = {16, 16, 8, 32, 32, 32, 16, 16, 16, 16, 8, 4, 2, 1, 0};
   return k[c];
 }
 __host__ __device__ constexpr uint32_t class_max_deg(int c) { return c == 0 ? 0xffffffffu : class_threads(c) * class_k(c); }
@@ -444,9 +448,14 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
         const uint64_t rb = ld_stream_u64(a.off + r, pf);
         d = static_cast<uint32_t>(ld_stream_u64(a.off + r + 1, pf) - rb);
         switch (class_k(c)) {
-          case 32:  // warp per row, 512 edges per pass (no block barrier)
-            for (uint32_t o = 0; o < d; o += 16 * 32) acc += gather_sum<16>(a, rb + o, d - o, l, 32, pf, pl);
+          case 32:
+            if (lanes == 32) {  // warp per row, 512 edges per pass (no block barrier)
+              for (uint32_t o = 0; o < d; o += 16 * 32) acc += gather_sum<16>(a, rb + o, d - o, l, 32, pf, pl);
+            } else {
+              acc = gather_sum<32>(a, rb, d, l, lanes, pf, pl);
+            }
             break;
+          case 64: acc = gather_sum<64>(a, rb, d, l, lanes, pf, pl); break;
           case 16: acc = gather_sum<16>(a, rb, d, l, lanes, pf, pl); break;
           case 8: acc = gather_sum<8>(a, rb, d, l, lanes, pf, pl); break;
           case 4: acc = gather_sum<4>(a, rb, d, l, lanes, pf, pl); break;
