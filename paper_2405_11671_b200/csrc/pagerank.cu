@@ -41,7 +41,9 @@
 namespace gbg {
 
 constexpr int kPrThreads = 256;
-constexpr uint32_t kChunk = 4096;  // edges per heavy-row chunk (16 per thread)
+// edges per heavy-row chunk (32 per thread, issued 8 at a time); 8192 beat
+// 2048 / 4096 / 16384 / 32768 at scales 20 and 24 (r01_pr_class_table.md)
+constexpr uint32_t kChunk = 8192;
 // Gathers of the kL1Hot highest-degree vertices (128 KiB of contribs, ~28%
 // of all gathers at scale 24) may stay in L1; the rest bypass it.
 #ifndef GBG_PR_L1HOT
@@ -51,7 +53,8 @@ constexpr uint32_t kL1Hot = GBG_PR_L1HOT;
 // Degree classes over the degree-descending rows: class c gives each row
 // T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
 // at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
-// 4096) splits rows into kChunk-edge chunks across CTAs; classes 1-2 (1025
+// 4096) splits rows into kChunk-edge chunks across CTAs (the class-0 K
+// entry is unused: a chunk gives each of the 256 threads kChunk/256 edges); classes 1-2 (1025
 // to 4096) take a CTA per row; class 3 (513 to 1024) a warp per row in two
 // 512-edge passes (no block barrier: better at scale 24, while the CTA form
 // stays better for the longer rows, which dominate at scale 20); below 513
@@ -451,11 +454,10 @@ __global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
           case 32:
             if (lanes == 32) {  // warp per row, 512 edges per pass (no block barrier)
               for (uint32_t o = 0; o < d; o += 16 * 32) acc += gather_sum<16>(a, rb + o, d - o, l, 32, pf, pl);
-            } else {
+            } else {  // (the table has K = 32 only, below a full warp)
               acc = gather_sum<32>(a, rb, d, l, lanes, pf, pl);
             }
             break;
-          case 64: acc = gather_sum<64>(a, rb, d, l, lanes, pf, pl); break;
           case 16: acc = gather_sum<16>(a, rb, d, l, lanes, pf, pl); break;
           case 8: acc = gather_sum<8>(a, rb, d, l, lanes, pf, pl); break;
           case 4: acc = gather_sum<4>(a, rb, d, l, lanes, pf, pl); break;
