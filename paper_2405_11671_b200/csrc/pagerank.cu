@@ -46,6 +46,9 @@ constexpr int kPrThreads = 256;
 constexpr uint32_t kChunk = 8192;
 // Gathers of the kL1Hot highest-degree vertices (128 KiB of contribs, ~28%
 // of all gathers at scale 24) may stay in L1; the rest bypass it.
+#ifndef GBG_PR_MINB
+#define GBG_PR_MINB 8  // CTAs of 256 per SM: the 32-register budget
+#endif
 #ifndef GBG_PR_L1HOT
 #define GBG_PR_L1HOT 16384
 #endif
@@ -383,7 +386,7 @@ __device__ __forceinline__ double gather_sum(const PrArgs& a, uint64_t b, uint32
 
 // Persistent: CTA b owns work units b, b + grid, ... (static assignment, so
 // the err / dangling fold is deterministic).
-__global__ void __launch_bounds__(kPrThreads, 8) pr_iter_k(PrArgs a) {
+__global__ void __launch_bounds__(kPrThreads, GBG_PR_MINB) pr_iter_k(PrArgs a) {
   __shared__ double s_red[33];
   __shared__ int s_flag;
   if (a.sc->done) return;
