@@ -57,8 +57,10 @@ constexpr uint32_t kL1Hot = GBG_PR_L1HOT;
 // T threads and each thread up to K edges, for degrees in (T*K/2, T*K], so
 // at most half of the unrolled, predicated slots are idle.  Class 0 (deg >
 // 4096) splits rows into kChunk-edge chunks across CTAs (the class-0 K
-// entry is unused: a chunk gives each of the 256 threads kChunk/256 edges); classes 1-2 (1025
-// to 4096) take a CTA per row; class 3 (513 to 1024) a warp per row in two
+// entry is unused: a chunk gives each of the 256 threads kChunk/256 edges);
+// class 1 (2049 to 4096) takes a CTA per row, class 2 (1025 to 2048) half a
+// CTA (4 warps x 16 edges per lane; s20 2.17 -> 2.11 ms, s24 unchanged);
+// class 3 (513 to 1024) a warp per row in two
 // 512-edge passes (no block barrier: better at scale 24, while the CTA form
 // stays better for the longer rows, which dominate at scale 20); below 513
 // edges a row gets 16 / 8 / 4 / 2 / 1 lanes walking 16-32 edges each in
@@ -68,11 +70,11 @@ constexpr uint32_t kL1Hot = GBG_PR_L1HOT;
 // (resolved analytically, not visited).
 constexpr int kClasses = 15;
 __host__ __device__ constexpr uint32_t class_threads(int c) {
-  constexpr uint32_t t[kClasses] = {256, 256, 256, 32, 16, 8, 8, 4, 2, 1, 1, 1, 1, 1, 1};
+  constexpr uint32_t t[kClasses] = {256, 256, 128, 32, 16, 8, 8, 4, 2, 1, 1, 1, 1, 1, 1};
   return t[c];
 }
 __host__ __device__ constexpr uint32_t class_k(int c) {
-  constexpr uint32_t k[kClasses] = {16, 16, 8, 32, 32, 32, 16, 16, 16, 16, 8, 4, 2, 1, 0};
+  constexpr uint32_t k[kClasses] = {16, 16, 16, 32, 32, 32, 16, 16, 16, 16, 8, 4, 2, 1, 0};
   return k[c];
 }
 __host__ __device__ constexpr uint32_t class_max_deg(int c) { return c == 0 ? 0xffffffffu : class_threads(c) * class_k(c); }
@@ -427,6 +429,28 @@ __global__ void __launch_bounds__(kPrThreads, GBG_PR_MINB) pr_iter_k(PrArgs a) {
         for (uint32_t k = 0; k < nch; ++k) tot += __ldcg(a.heavy_partial + c0 + k);
         pr_finalize(a, base, r, re - rb, tot, err);
         a.heavy_counter[r] = 0;
+      }
+      __syncthreads();
+    } else if (class_threads(c) == kPrThreads / 2) {
+      // ---- half a CTA (4 warps) per row, two rows per unit
+      const uint32_t half = threadIdx.x >> 7, t = threadIdx.x & 127;
+      const uint64_t r64 = a.row_begin[c] + static_cast<uint64_t>(w - a.unit_begin[c]) * 2 + half;
+      const bool valid = r64 < a.row_begin[c + 1];
+      const uint32_t r = static_cast<uint32_t>(r64);
+      double p = 0.0;
+      uint32_t d = 0;
+      if (valid) {
+        const uint64_t rb = __ldg(a.off + r);
+        d = static_cast<uint32_t>(__ldg(a.off + r + 1) - rb);
+        if (class_k(c) == 32) p = gather_sum<32>(a, rb, d, t, 128, pf, pl);
+        else p = gather_sum<16>(a, rb, d, t, 128, pf, pl);
+      }
+      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = p;
+      __syncthreads();
+      if (t == 0 && valid) {
+        const double s = (s_red[4 * half] + s_red[4 * half + 1]) + (s_red[4 * half + 2] + s_red[4 * half + 3]);
+        pr_finalize(a, base, r, d, s, err);
       }
       __syncthreads();
     } else if (class_threads(c) == kPrThreads) {
