@@ -537,11 +537,6 @@ __global__ void pr_init_k(const uint64_t* off, uint64_t n, double* x, double* x1
   }
 }
 
-struct DanglingIn {
-  const uint64_t* off;
-  double p0;
-  __device__ __forceinline__ double operator()(uint64_t r) const { return off[r + 1] - off[r] ? 0.0 : p0; }
-};
 
 // p[old id] from the contrib form of the renumbered vector (zero-degree
 // rows: the rank of the last executed iteration, sc->p_zero)
@@ -556,8 +551,8 @@ __global__ void pr_to_p_k(const uint64_t* off, const uint32_t* pos, uint64_t n, 
   }
 }
 
-__global__ void pr_scalars_init_k(PrScalars* sc, const double* dangling0, double p0) {
-  sc->dangling[0] = *dangling0;
+__global__ void pr_scalars_init_k(PrScalars* sc, double dangling0, double p0) {
+  sc->dangling[0] = dangling0;
   sc->dangling[1] = 0.0;
   sc->p_zero = p0;
   sc->err = 0.0;
@@ -595,12 +590,12 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
   PrLayout* L = pr_layout(g);
   double* X0 = g->ws.get<double>("pr.x0", n);
   double* X1 = g->ws.get<double>("pr.x1", n);
-  double* d0 = g->ws.get<double>("pr.d0", 1);
   PrScalars* sc = g->ws.get<PrScalars>("pr.sc", 1);
   const double p0 = 1.0 / static_cast<double>(n);
   GBG_LAUNCH(g, pr_init_k, grid_for(n, 256), 256, 0, L->off, n, X0, X1);
-  device_scan<double>(g, DanglingIn{L->off, p0}, NullOut{}, n, d0, "pr.dang");
-  GBG_LAUNCH(g, pr_scalars_init_k, 1, 1, 0, sc, d0, p0);
+  // initial dangling mass: every zero-degree row holds p0
+  const double n_zero = static_cast<double>(n - L->row_begin[kClasses - 1]);
+  GBG_LAUNCH(g, pr_scalars_init_k, 1, 1, 0, sc, n_zero * p0, p0);
   double* X[2] = {X0, X1};
   for (uint64_t it = 0; it < max_iters; ++it) {
     PrArgs a;
