@@ -234,6 +234,19 @@ class Ref:
         L.gbref_csr_free(h)
         return n, off, nbr[:m]
 
+    def load_binary_graph(self, path):
+        """gb::load_binary_csr (io.cpp:87-110), kept as a reference CsrGraph
+        (the input path bench.cpp uses for cached graphs)."""
+        L = self.L
+        L.gbref_load_binary.restype = C.c_void_p
+        L.gbref_load_binary.argtypes = [C.c_char_p]
+        L.gbref_csr_n.restype = C.c_uint64
+        L.gbref_csr_n.argtypes = [C.c_void_p]
+        h = L.gbref_load_binary(os.fsencode(path))
+        if not h:
+            raise RefError(L.gbref_last_error().decode())
+        return RefCsr(self, h, int(L.gbref_csr_n(h)))
+
     def prepare_global(self, pairs):
         pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.uint32).reshape(-1, 2))
         out = np.empty_like(pairs)
@@ -260,6 +273,13 @@ class RefCsr:
         except Exception:
             pass
 
+    @property
+    def m(self):
+        L = self.ref.L
+        L.gbref_csr_m.restype = C.c_uint64
+        L.gbref_csr_m.argtypes = [C.c_void_p]
+        return int(L.gbref_csr_m(self.h))
+
     def bfs(self, src):
         out = np.empty(self.n, dtype=np.int32)
         self.ref._check(self.ref.L.gbref_bfs(self.h, src, ptr(out, _i32p)))
@@ -284,6 +304,29 @@ class RefCsr:
         out = np.empty(self.n, dtype=np.float64)
         self.ref._check(self.ref.L.gbref_pagerank(self.h, damping, iters, tol, ptr(out, _f64p)))
         return out
+
+    def time_pagerank(self, damping=0.85, iters=20, tol=np.finfo(np.float64).tiny):
+        """Seconds of one gb::pagerank call (steady_clock inside the shim) and
+        the rank sum."""
+        L = self.ref.L
+        L.gbref_time_pagerank.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_double, _f64p, _f64p]
+        sec, tot = C.c_double(), C.c_double()
+        self.ref._check(L.gbref_time_pagerank(self.h, damping, iters, tol, C.byref(sec), C.byref(tot)))
+        return sec.value, tot.value
+
+    def time_bfs(self, src):
+        L = self.ref.L
+        L.gbref_time_bfs.argtypes = [C.c_void_p, C.c_uint32, _f64p, _u64p]
+        sec, k = C.c_double(), C.c_uint64()
+        self.ref._check(L.gbref_time_bfs(self.h, src, C.byref(sec), C.byref(k)))
+        return sec.value, k.value
+
+    def time_cc(self):
+        L = self.ref.L
+        L.gbref_time_cc.argtypes = [C.c_void_p, _f64p, _u64p]
+        sec, k = C.c_double(), C.c_uint64()
+        self.ref._check(L.gbref_time_cc(self.h, C.byref(sec), C.byref(k)))
+        return sec.value, k.value
 
     def cc(self):
         out = np.empty(self.n, dtype=np.uint32)
@@ -399,6 +442,23 @@ class RefChunked:
                                                        C.byref(applied)))
         return applied.value
 
+    def apply_timed(self, pairs, insert: bool):
+        """(applied, seconds of prepare + apply) as bench.cpp:171-186 times them."""
+        L = self.ref.L
+        L.gbref_chunked_apply_timed.argtypes = [C.c_void_p, _u32p, C.c_uint64, C.c_int, _u64p, _f64p]
+        pairs = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        applied, sec = C.c_uint64(0), C.c_double()
+        self.ref._check(L.gbref_chunked_apply_timed(self.h, ptr(pairs, _u32p), pairs.shape[0], int(insert),
+                                                    C.byref(applied), C.byref(sec)))
+        return applied.value, sec.value
+
+    def time_bfs(self, src):
+        L = self.ref.L
+        L.gbref_container_bfs_timed.argtypes = [C.c_void_p, C.c_uint32, _f64p, _u64p]
+        sec, k = C.c_double(), C.c_uint64()
+        self.ref._check(L.gbref_container_bfs_timed(self.h, src, C.byref(sec), C.byref(k)))
+        return sec.value, k.value
+
     def export(self):
         off = np.empty(self.n + 1, dtype=np.uint64)
         nbr = np.empty(self.m, dtype=np.uint32)
@@ -446,6 +506,33 @@ class Oracle:
                                    _u64p]
         L.gbo_set_apply.restype = C.c_uint64
         L.gbo_set_apply.argtypes = [C.c_uint64, _u64p, _u32p, _u32p, C.c_uint64, C.c_int, _u64p, _u32p]
+
+    def rmat_csr(self, log2_n, draws, seed, a=RMAT_A, b=RMAT_B, c=RMAT_C):
+        """generate_rmat (generators.cpp:67-72) as (offsets, neighbours),
+        OpenMP on every host core (oracle/gbo_omp.c)."""
+        L = self.L
+        L.gbo_rmat_csr_omp.restype = C.c_uint64
+        L.gbo_rmat_csr_omp.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
+                                       _u64p, C.POINTER(_u32p)]
+        L.gbo_free.argtypes = [C.c_void_p]
+        n = 1 << log2_n
+        off = np.empty(n + 1, dtype=np.uint64)
+        p = _u32p()
+        m = L.gbo_rmat_csr_omp(log2_n, a, b, c, draws, seed, ptr(off, _u64p), C.byref(p))
+        if m == (1 << 64) - 1:
+            raise MemoryError("gbo_rmat_csr_omp: out of host memory")
+        nbr = np.ctypeslib.as_array(p, shape=(max(m, 1),))[:m].copy()
+        L.gbo_free(C.cast(p, C.c_void_p))
+        return off, nbr
+
+    def save_gbcsr1(self, path, n, off, nbr):
+        """GBCSR1 file as gb::save_binary writes it (io.cpp:75-85)."""
+        L = self.L
+        L.gbo_save_gbcsr1.argtypes = [C.c_char_p, C.c_uint64, _u64p, _u32p]
+        off = np.ascontiguousarray(off, dtype=np.uint64)
+        nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
+        if L.gbo_save_gbcsr1(os.fsencode(path), n, ptr(off, _u64p), ptr(nbr if nbr.size else np.zeros(1, np.uint32), _u32p)):
+            raise OSError(f"cannot write {path}")
 
     def update_batch(self, log2_n, size, seed, a=RMAT_A, b=RMAT_B, c=RMAT_C):
         out = np.empty((2 * size, 2), dtype=np.uint32)

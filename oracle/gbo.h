@@ -48,4 +48,9 @@ int gbo_edge_map(uint64_t n, const uint64_t* off, const uint32_t* nbr, const uin
 
 uint64_t gbo_set_apply(uint64_t n, const uint64_t* off, const uint32_t* nbr, const uint32_t* batch,
                        uint64_t bcount, int insert, uint64_t* off_out, uint32_t* nbr_out);
+/* gbo_omp.c: OpenMP R-MAT generator straight into CSR, GBCSR1 writer */
+uint64_t gbo_rmat_csr_omp(uint64_t log2_n, double a, double b, double c, uint64_t draws, uint64_t seed,
+                          uint64_t* off, uint32_t** nbr_out);
+void gbo_free(void* p);
+int gbo_save_gbcsr1(const char* path, uint64_t n, const uint64_t* off, const uint32_t* nbr);
 #endif

@@ -32,6 +32,7 @@
 // gbref_last_error().
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -454,6 +455,76 @@ int gbref_container_bfs(void* c, uint32_t src, int32_t* depth) {
     BfsResult r = bfs(view, src);
     for (size_t v = 0; v < r.distances.size(); ++v)
       depth[v] = r.distances[v] == kInfiniteDistance ? -1 : static_cast<int32_t>(r.distances[v]);
+  });
+}
+
+// ---- timed calls for bench.py's CPU legs: steady_clock around the
+// reference call alone, as bench.cpp times a trial (bench.cpp:88-103) and
+// an update (prepare + apply, bench.cpp:171-186); conversions stay outside
+namespace {
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+int gbref_time_pagerank(void* csr, double damping, uint64_t iters, double tol, double* seconds,
+                        double* rank_sum) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<double> p = pagerank(view, damping, iters, tol);
+    *seconds = seconds_since(t0);
+    double s = 0.0;
+    for (double x : p) s += x;
+    *rank_sum = s;
+  });
+}
+
+int gbref_time_bfs(void* csr, uint32_t src, double* seconds, uint64_t* reached) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    auto t0 = std::chrono::steady_clock::now();
+    BfsResult r = bfs(view, src);
+    *seconds = seconds_since(t0);
+    uint64_t k = 0;
+    for (uint64_t d : r.distances) k += d != kInfiniteDistance;
+    *reached = k;
+  });
+}
+
+int gbref_time_cc(void* csr, double* seconds, uint64_t* components) {
+  return guard([&] {
+    GraphView view(*static_cast<CsrGraph*>(csr));
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<VertexId> l = cc(view);
+    *seconds = seconds_since(t0);
+    uint64_t k = 0;
+    for (size_t v = 0; v < l.size(); ++v) k += l[v] == v;
+    *components = k;
+  });
+}
+
+int gbref_chunked_apply_timed(void* c, const uint32_t* pairs, uint64_t count, int insert, uint64_t* applied,
+                              double* seconds) {
+  return guard([&] {
+    GraphContainer& g = *static_cast<GraphContainer*>(c);
+    EdgeBatch eb{pairs_to_edges(pairs, count)};
+    auto t0 = std::chrono::steady_clock::now();
+    PreparedBatch pb = prepare(eb, g.preferred_batch_form());
+    *applied = insert ? apply_insert(g, pb) : apply_delete(g, pb);
+    *seconds = seconds_since(t0);
+  });
+}
+
+int gbref_container_bfs_timed(void* c, uint32_t src, double* seconds, uint64_t* reached) {
+  return guard([&] {
+    GraphView view(*static_cast<GraphContainer*>(c));
+    auto t0 = std::chrono::steady_clock::now();
+    BfsResult r = bfs(view, src);
+    *seconds = seconds_since(t0);
+    uint64_t k = 0;
+    for (uint64_t d : r.distances) k += d != kInfiniteDistance;
+    *reached = k;
   });
 }
 

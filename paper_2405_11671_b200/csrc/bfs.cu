@@ -17,6 +17,7 @@
 #include <memory>
 #include <vector>
 
+#include "edges.cuh"
 #include "traverse.cuh"
 
 #ifndef GBG_BFS_SMALL_GRID
@@ -403,7 +404,7 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
   s.src = src;
   s.first = first_neighbors(g);
-  s.iso = isolated_bitmap(g);
+  s.iso = bfs_premark(g);
   void* args[] = {&view, &s};
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));
@@ -435,7 +436,7 @@ void bfs_run(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* 
   TraversalBuffers tb(g);
   uint32_t* visited = g->ws.get<uint32_t>("bfs.visited", tb.nw + 2);
   GBG_CUDA(cudaMemsetAsync(depth, 0xff, g->n * sizeof(int32_t), g->stream));
-  GBG_CUDA(cudaMemcpyAsync(visited, isolated_bitmap(g), tb.nw * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+  GBG_CUDA(cudaMemcpyAsync(visited, bfs_premark(g), tb.nw * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
                            g->stream));
   GBG_CUDA(cudaMemsetAsync(tb.a.bm, 0, tb.nw * sizeof(uint32_t), g->stream));
   GBG_LAUNCH(g, bfs_init_k<G>, 1, 1, 0, view, src, visited, depth, tb.a.list, tb.a.dscan, tb.a.bm, tb.packed);
@@ -587,6 +588,32 @@ const uint64_t* first_neighbors(gbg_graph* g) {
   return g->first;
 }
 const uint32_t* isolated_bitmap(gbg_graph* g) { return reinterpret_cast<const uint32_t*>(first_neighbors(g) + g->n); }
+
+namespace {
+struct ClearTargetOp {
+  uint32_t* bm;
+  __device__ __forceinline__ void operator()(uint32_t, uint32_t v, uint64_t) const {
+    atomicAnd(bm + (v >> 5), ~(1u << (v & 31)));
+  }
+};
+}  // namespace
+
+// The visited bits a BFS may set before it starts: vertices no level can
+// reach.  A sparse level reaches v through an arc u -> v (traversal.cpp:
+// 16-46 walks u's list); a dense level through v's own list (traversal.cpp:
+// 48-95 scans N(v) for a frontier member).  So only vertices with neither
+// in-arcs nor out-arcs are unreachable.  On a symmetric graph those are the
+// zero-degree vertices (the cached isolated bitmap); on a directed graph
+// the isolated bitmap minus every arc target, built per call.
+const uint32_t* bfs_premark(gbg_graph* g) {
+  if (graph_is_symmetric(g)) return isolated_bitmap(g);
+  const uint64_t nw = (g->n + 31) / 32;
+  uint32_t* bm = g->ws.get<uint32_t>("bfs.premark", nw + 1);
+  GBG_CUDA(cudaMemcpyAsync(bm, isolated_bitmap(g), nw * sizeof(uint32_t), cudaMemcpyDeviceToDevice, g->stream));
+  const uint64_t* voff = virtual_offsets(g);
+  with_view(g, [&](auto view) { for_each_edge(g, view, voff, g->m, ClearTargetOp{bm}); });
+  return bm;
+}
 }  // namespace gbg
 
 using namespace gbg;

@@ -140,7 +140,9 @@ __global__ void make_keys_k(const uint32_t* pairs, uint64_t count, uint64_t n, B
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
     const uint32_t s = pairs[2 * i], d = pairs[2 * i + 1];
-    const bool oor = s >= n || d >= n;
+    // prepare(GlobalSort) drops self-loops before anything looks at the ids
+    // (batch.cpp:34-42), so only a non-loop arc can be out of range
+    const bool oor = s != d && (s >= n || d >= n);
     if (oor) *bad = 1;
     // self-loops (and out-of-range arcs, which fail the call before any
     // change) become the all-ones key, itself a self-loop, dropped below
@@ -178,11 +180,28 @@ __global__ void contains_k(G g, const uint32_t* pairs, uint64_t count, uint8_t* 
 // presence of each prepared arc in the container (flag = changes the
 // container: absent for insert, present for delete) and its rank among the
 // source's current neighbours (the merge slot offset of an inserted arc)
+//
+// With check_sym (the container is symmetric before the batch) it also
+// checks that the batch is closed under reversal: every unique (s, d) with
+// s < d finds (d, s) among the unique keys, and the s < d and s > d counts
+// agree.  A symmetric batch applied to a symmetric container leaves it
+// symmetric (an arc is absent/present iff its reverse is), so BFS keeps
+// the cached zero-degree pre-mark after R-MAT batches (bfs_premark).
+__device__ __forceinline__ bool has_key(const uint64_t* k, uint64_t U, uint64_t x) {
+  uint64_t lo = 0, hi = U;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (k[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo < U && k[lo] == x;
+}
 __global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t* U_dev, BatchKeys bk,
                               const uint64_t* start, const uint32_t* deg, const uint32_t* pool, int insert,
-                              uint32_t* flag, uint32_t* lb) {
+                              uint32_t* flag, uint32_t* lb, int check_sym, int* asym, uint64_t* lt,
+                              uint64_t* gt) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t U = *U_dev;
+  uint32_t nlt = 0, ngt = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
     if (i >= U) break;
     const uint64_t x = k[i];
@@ -193,6 +212,22 @@ __global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t*
     const bool present = pos < len && lst[pos] == d;
     flag[i] = insert ? !present : present;
     lb[i] = pos;
+    if (check_sym) {
+      if (s < d) {
+        ++nlt;
+        if (!has_key(k, U, bk.make(d, s))) *asym = 1;
+      } else {
+        ++ngt;
+      }
+    }
+  }
+  if (check_sym) {
+    nlt = __reduce_add_sync(0xffffffffu, nlt);
+    ngt = __reduce_add_sync(0xffffffffu, ngt);
+    if ((threadIdx.x & 31) == 0) {
+      if (nlt) atomicAdd(reinterpret_cast<unsigned long long*>(lt), nlt);
+      if (ngt) atomicAdd(reinterpret_cast<unsigned long long*>(gt), ngt);
+    }
   }
 }
 struct ApplyOut {
@@ -374,6 +409,8 @@ struct UpdScalars {
   uint32_t ng;    // touched sources
   int bad;        // an endpoint >= n
   int under;      // metadata underflow
+  int asym;       // a unique arc (s, d), s < d, whose reverse is not in the batch
+  uint64_t lt, gt;  // unique arcs with s < d / s > d
 };
 
 // Grow the pool when the batch's allocations do not fit (rare): the live
@@ -419,7 +456,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint32_t* lb = g->ws.get<uint32_t>("upd.lb", count);
   uint32_t* alb = g->ws.get<uint32_t>("upd.alb", count);
   GBG_LAUNCH(g, apply_flags_k, grid_for(count, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk, g->bstart,
-             g->bdeg, g->pool, insert ? 1 : 0, flag, lb);
+             g->bdeg, g->pool, insert ? 1 : 0, flag, lb, g->symmetric ? 1 : 0, &sc->asym, &sc->lt, &sc->gt);
   device_scan<uint32_t>(g, BoundedIn<uint32_t, uint64_t>{flag, &sc->U}, ApplyOut{flag, &sc->U, ukeys, lb, akeys, alb},
                         count, &sc->A, "upd.apply");
   // groups by source
@@ -473,8 +510,11 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
     g->m -= A;
   }
   g->invalidate_derived();
-  g->symmetric = false;  // arbitrary batches need not keep arc pairs: re-verify lazily
-  g->sym_checked = false;
+  // a symmetric batch keeps a symmetric container symmetric; anything else
+  // is re-verified lazily (graph_is_symmetric)
+  const bool keeps = g->symmetric && !h.asym && h.lt == h.gt;
+  g->symmetric = keeps;
+  g->sym_checked = keeps;
   return A;
 }
 

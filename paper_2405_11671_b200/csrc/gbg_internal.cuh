@@ -266,6 +266,8 @@ inline bool coop_enabled(int device) {
 const uint64_t* first_neighbors(gbg_graph* g);
 // Bit v set when v has no neighbours (same lifetime as first_neighbors).
 const uint32_t* isolated_bitmap(gbg_graph* g);
+// Vertices no arc points to (the visited bits a BFS starts with; bfs.cu).
+const uint32_t* bfs_premark(gbg_graph* g);
 
 // Every arc has its reverse (checked once per graph version, cc.cu).
 bool graph_is_symmetric(gbg_graph* g);

@@ -22,7 +22,8 @@ struct BatchKeys {
   }
   // self-loops are encoded as this key (itself a self-loop) and dropped
   __host__ __device__ __forceinline__ uint64_t loop_key() const {
-    return make((1u << L) - 1, (1u << L) - 1);
+    const uint32_t all = static_cast<uint32_t>((uint64_t{1} << L) - 1);  // L may be 32
+    return make(all, all);
   }
 };
 

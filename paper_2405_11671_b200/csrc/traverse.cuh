@@ -667,7 +667,7 @@ __device__ __forceinline__ void emit_warp(G g, bool emit, uint32_t v, uint32_t* 
 
 // Sparse push straight from a frontier bitmap (the dense -> sparse
 // transition), with no id list or degree prefix built first: each warp
-// takes strided batches of up to 8 frontier words, packs the batch's
+// takes strided batches of up to kPushBatch (16) frontier words, packs the batch's
 // members onto the lanes 32 per round, and every lane walks its member's
 // list in lock-step with the warp (one step = one neighbour per lane, an
 // aggregated emission per step); lists longer than kPullSerial finish

@@ -484,6 +484,11 @@ def pagerank(g: _Graph, damping: float = 0.85, max_iters: int = 20, tolerance: f
     return out
 
 
+def pagerank_kernel_name() -> str:
+    """Name of the per-iteration PageRank kernel (for ncu lookups)."""
+    return "pr_tile_k"
+
+
 def pagerank_prepare(g: _Graph) -> float:
     """Build the cached degree-ordered PageRank layout; returns its build ms."""
     ms = C.c_double()

@@ -18,6 +18,7 @@ At S=22 also the config-5 update sequence on the reference "chunked_set"
 container (see `updates()`).
 
     python tests/golden/make_golden.py --greedy 16 20 24
+    python tests/golden/make_golden.py --updates 22   # config 5, reps 0..2
 
 adds (in place) the priority-order consumers of §8(f) row 3:
   kcore      digest(uint64 coreness), max coreness
@@ -69,11 +70,13 @@ def update_seed(ref, size, rep):
     return ref.hash_combine(ref.hash_combine(2, size), rep)
 
 
-def updates(ref, n, off, nbr, S):
+def updates(ref, n, off, nbr, S, reps=3):
     """Config 5 on the reference dynamic container ("chunked_set",
-    registry.cpp:136-137): per size (rep 0) sample a batch, drop arcs already
-    in the base (bench.cpp:150-169 policy, untimed), insert (prepare +
-    apply_insert), BFS from the lowest-id max-degree vertex, delete."""
+    registry.cpp:136-137), in run_updates' order (bench.cpp:158-187): per
+    size and rep 0..2 sample a batch with seed hash_combine(hash_combine(2,
+    size), rep), drop arcs already in the base (bench.cpp:150-169 policy,
+    untimed), insert (prepare + apply_insert), BFS from the lowest-id
+    max-degree vertex, delete."""
     src_of = np.repeat(np.arange(n, dtype=np.uint64), np.diff(off.astype(np.int64)))
     base_keys = (src_of << np.uint64(32)) | nbr.astype(np.uint64)
     del src_of
@@ -83,8 +86,8 @@ def updates(ref, n, off, nbr, S):
     del pairs
     print(f"s{S}: chunked_set built in {time.time() - t:.1f}s", flush=True)
     out = []
-    for size in UPDATE_SIZES:
-        seed = update_seed(ref, size, 0)
+    for size, rep in [(size, rep) for size in UPDATE_SIZES for rep in range(reps)]:
+        seed = update_seed(ref, size, rep)
         raw = ref.update_batch(S, size, seed)
         keys = (raw[:, 0].astype(np.uint64) << np.uint64(32)) | raw[:, 1].astype(np.uint64)
         keep = ~np.isin(keys, base_keys)
@@ -96,7 +99,7 @@ def updates(ref, n, off, nbr, S):
         src = max_degree_source(eo)
         depth = cont.bfs(src)
         dele = cont.apply(fresh, False)
-        rec = dict(size=size, seed=seed, raw_digest=digest(raw.reshape(-1)), fresh=int(fresh.shape[0]),
+        rec = dict(size=size, rep=rep, seed=seed, raw_digest=digest(raw.reshape(-1)), fresh=int(fresh.shape[0]),
                    fresh_digest=digest(fresh.reshape(-1)), inserted=ins, m_after_insert=m_ins,
                    off_digest_after_insert=digest(eo), nbr_digest_after_insert=digest(en), bfs_source=src,
                    bfs_digest=digest(depth), bfs_reached=int((depth >= 0).sum()), deleted=dele,
@@ -177,8 +180,23 @@ def greedy(scales):
             json.dump(rec, f, indent=1)
 
 
+def refresh_updates(S=22):
+    """Recompute only the config-5 update sequence of rmat_s{S}.json."""
+    ref = Ref()
+    n, off, nbr = graph(ref, S)
+    path = os.path.join(HERE, f"rmat_s{S}.json")
+    with open(path) as f:
+        rec = json.load(f)
+    assert rec["m"] == int(off[n])
+    rec["updates"] = updates(ref, n, off, nbr, S)
+    with open(path, "w") as f:
+        json.dump(rec, f, indent=1)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:2] == ["--greedy"]:
+    if sys.argv[1:2] == ["--updates"]:
+        refresh_updates(int(sys.argv[2]) if len(sys.argv) > 2 else 22)
+    elif sys.argv[1:2] == ["--greedy"]:
         greedy([int(x) for x in sys.argv[2:]])
     else:
         main([int(x) for x in sys.argv[1:]] or [16, 20])

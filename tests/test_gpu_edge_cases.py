@@ -260,3 +260,68 @@ def test_concurrent_reads_from_threads(gbg, orc):
     for t in threads:
         t.join()
     assert not errors, errors[:3]
+
+
+def _directed_with_sinks(n, p, sink_frac, seed):
+    """Random directed arcs, then every out-arc of a `sink_frac` share of the
+    vertices removed: those vertices keep in-arcs but have degree 0."""
+    rng = np.random.default_rng(seed)
+    a = rng.random((n, n)) < p
+    np.fill_diagonal(a, False)
+    a[rng.random(n) < sink_frac, :] = False
+    s, d = np.nonzero(a)
+    return np.stack([s, d], axis=1).astype(np.uint32)
+
+
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
+def test_directed_bfs_reaches_vertices_without_out_arcs(gbg, ref, kind):
+    """A vertex with in-arcs but no out-arcs is reached by a sparse push
+    (traversal.cpp:16-46 walks the frontier member's list); it must not be
+    pre-marked visited as a zero-degree vertex of a symmetric graph would
+    be.  First the advisor's case (arc 0->1 plus a 30-clique: bfs(0) gives
+    depth[1] = 1), then seeded directed graphs with sinks and BC on them."""
+    mk = gbg.CsrGraph.build if kind == "csr" else gbg.BlockedGraph.build
+    arcs = [(0, 1)] + [(i, j) for i in range(2, 32) for j in range(2, 32) if i != j]
+    pairs = np.array(sorted(arcs), dtype=np.uint32)
+    off, nbr = csr(32, pairs)
+    g = mk(32, pairs)
+    r = gbg.bfs(g, 0)
+    assert np.array_equal(r.depth, ref.csr(32, off, nbr).bfs(0))
+    assert r.depth[1] == 1
+    for seed, (n, p) in enumerate([(300, 0.02), (2000, 0.004), (2000, 0.03)]):
+        pairs = _directed_with_sinks(n, p, 0.3, seed)
+        off, nbr = csr(n, pairs)
+        rg = ref.csr(n, off, nbr)
+        g = mk(n, pairs)
+        for src in (0, 1, n // 2, n - 1):
+            assert np.array_equal(gbg.bfs(g, src).depth, rg.bfs(src)), (seed, src)
+        for src in (0, n // 3):
+            want = rg.bc(src)
+            assert np.allclose(gbg.bc(g, src), want, rtol=1e-12, atol=1e-12, equal_nan=True), (seed, src)
+
+
+def test_symmetric_batches_keep_the_premark(gbg, ref, orc):
+    """Insert/delete of a reverse-closed batch keeps the blocked container
+    symmetric; a one-directional arc makes it asymmetric, and BFS then
+    still reaches the new sink (checked against the reference)."""
+    n = 64
+    nn, pairs = undirected(n, [(i, (i * 7 + 3) % n) for i in range(n)], orc)
+    g = gbg.BlockedGraph.build(nn, pairs)
+    g.insert_batch(np.array([[1, 40], [40, 1], [5, 6], [6, 5]], dtype=np.uint32))
+    g.delete_batch(np.array([[1, 40], [40, 1]], dtype=np.uint32))
+    g.insert_batch(np.array([[2, 63]], dtype=np.uint32))  # one direction only
+    off, nbr = g.to_csr()
+    rg = ref.csr(nn, off, nbr)
+    for src in range(0, n, 7):
+        assert np.array_equal(gbg.bfs(g, src).depth, rg.bfs(src))
+
+
+def test_batch_self_loop_with_out_of_range_id_is_dropped(gbg, ref):
+    """prepare(GlobalSort) drops self-loops before any id check
+    (batch.cpp:34-42), so (n+5, n+5) is ignored, not an out-of-range error;
+    a non-loop out-of-range arc still fails."""
+    g = gbg.BlockedGraph.build(4, np.array([[0, 1], [1, 0]], dtype=np.uint32))
+    assert g.insert_batch(np.array([[9, 9], [2, 3], [3, 2]], dtype=np.uint32)) == 2
+    assert g.num_edges() == 4
+    with pytest.raises(IndexError):
+        g.insert_batch(np.array([[2, 9]], dtype=np.uint32))

@@ -54,6 +54,34 @@ def test_rmat_s16_matches_golden(orc):
     assert digest(off) == gd["off_digest"] and digest(nbr) == gd["nbr_digest"]
 
 
+@pytest.mark.parametrize("S,seed,abc", [(1, 1, (0.57, 0.19, 0.19)), (10, 1, (0.57, 0.19, 0.19)),
+                                         (14, 1, (0.57, 0.19, 0.19)), (12, 42, (0.5, 0.1, 0.1)),
+                                         (13, 7, (0.45, 0.15, 0.25))])
+def test_parallel_rmat_csr_matches_reference(ref, orc, S, seed, abc):
+    """oracle/gbo_omp.c (the bench's host-side generator for the CPU
+    reference arm) against gb::generate_rmat + CsrGraph::build."""
+    n, pairs = ref.rmat(S, 16 << S, seed, *abc)
+    want_off, want_nbr = csr(n, pairs)
+    off, nbr = orc.rmat_csr(S, 16 << S, seed, *abc)
+    assert np.array_equal(off, want_off) and np.array_equal(nbr, want_nbr)
+
+
+def test_parallel_rmat_s16_golden_and_gbcsr1_bytes(ref, orc, tmp_path):
+    """Scale 16 against the golden digests, and the GBCSR1 writer against
+    gb::save_binary byte for byte; gb::load_binary_csr reads it back."""
+    gd = golden(16)
+    off, nbr = orc.rmat_csr(16, 16 << 16, 1)
+    assert digest(off) == gd["off_digest"] and digest(nbr) == gd["nbr_digest"]
+    n = off.size - 1
+    ours, theirs = tmp_path / "ours.gbcsr1", tmp_path / "ref.gbcsr1"
+    orc.save_gbcsr1(str(ours), n, off, nbr)
+    ref.csr(n, off, nbr).save_binary(str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()
+    g = ref.load_binary_graph(str(ours))
+    assert g.n == n
+    assert np.array_equal(g.bfs(0), ref.csr(n, off, nbr).bfs(0))
+
+
 def test_normalize_and_fixture(ref, orc):
     n, p = ref.t4()
     assert n == 4 and np.array_equal(p, T4_PAIRS)
