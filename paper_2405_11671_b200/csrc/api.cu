@@ -268,19 +268,19 @@ gbg_status gbg_csr_create_ex(uint64_t n, uint64_t m, const uint64_t* offsets, co
     int hb = 0;
     read_scalars(g, bad, sizeof(int), &hb);
     if (hb) fail(GBG_ERR_FORMAT, "csr_build: offsets must rise monotonically from 0 to m");
-    PrLayout* L = nullptr;
+    prrows::PrRows* L = nullptr;
     struct LayoutHold {
-      PrLayout*& L;
+      prrows::PrRows*& L;
       ~LayoutHold() {
-        if (L) pr_layout_free(L);
+        if (L) prrows::pr_layout_free(L);
       }
     } lh{L};
-    if ((flags & GBG_CREATE_PAGERANK_LAYOUT) && n) L = pr_layout_rows_csr(g);  // offsets only
+    if ((flags & GBG_CREATE_PAGERANK_LAYOUT) && n) L = prrows::pr_layout_rows_csr(g);  // offsets only
     for (uint64_t c = 0; c < nchunks; ++c) {
       const uint64_t e0 = c * kChunkIds, e1 = std::min(m, e0 + kChunkIds);
       GBG_CUDA(cudaStreamWaitEvent(g->stream, cp.ev[c + 1], 0));
       for_each_edge_range(g, g->csr_view(), g->off, e0, e1, SegmentOrderOp{g->off, g->nbr, n, bad});
-      if (L) pr_layout_relabel_csr(g, L, e0, e1);
+      if (L) prrows::pr_layout_relabel_csr(g, L, e0, e1);
     }
     GBG_CUDA(cudaEventRecord(t1, g->stream));
     read_scalars(g, bad, sizeof(int), &hb);
@@ -290,7 +290,7 @@ gbg_status gbg_csr_create_ex(uint64_t n, uint64_t m, const uint64_t* offsets, co
     cudaEventDestroy(t1);
     if (hb) fail(GBG_ERR_FORMAT, "csr_build: arcs must be sorted, deduplicated and in range");
     if (L) {
-      pr_layout_attach(g, L, ms);
+      prrows::pr_layout_attach(g, L, ms);
       L = nullptr;
     }
     *out = hold.release();

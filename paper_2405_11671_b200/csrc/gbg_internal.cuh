@@ -148,7 +148,10 @@ struct BlockedView {
 };
 
 // ---------------------------------------------------------------- handle
-struct PrLayout;  // pagerank.cu
+struct PrLayout;  // pagerank.cu (tiled index)
+namespace prrows {
+struct PrRows;  // pagerank_rows.cu (row path)
+}
 struct TcCache;     // tc.cu
 
 }  // namespace gbg
@@ -194,7 +197,8 @@ struct gbg_graph {
   bool voff_valid = false;
   uint64_t* first = nullptr;   // (degree << 32) | first neighbour of every vertex (kNoFirst if isolated) + isolated bitmap
   bool first_valid = false;
-  gbg::PrLayout* pr = nullptr;  // cached degree-ordered PageRank layout
+  gbg::PrLayout* pr = nullptr;          // cached PageRank tiled index (gbg_pagerank_prepare)
+  gbg::prrows::PrRows* pr_rows = nullptr;  // cached PageRank row layout (one-shot path)
 
   gbg::Workspace ws;
   // pinned host staging for small device->host reads (scalars, per-level stats)
@@ -273,10 +277,15 @@ const uint32_t* bfs_premark(gbg_graph* g);
 bool graph_is_symmetric(gbg_graph* g);
 
 // PageRank layout in phases for pipelined CSR builds (pagerank.cu).
-PrLayout* pr_layout_rows_csr(gbg_graph* g);
-void pr_layout_relabel_csr(gbg_graph* g, PrLayout* L, uint64_t e0, uint64_t e1);
-void pr_layout_attach(gbg_graph* g, PrLayout* L, float build_ms);
-void pr_layout_free(PrLayout* L);
+namespace prrows {
+PrRows* pr_layout_rows_csr(gbg_graph* g);
+void pr_layout_relabel_csr(gbg_graph* g, PrRows* L, uint64_t e0, uint64_t e1);
+void pr_layout_attach(gbg_graph* g, PrRows* L, float build_ms);
+void pr_layout_free(PrRows* L);
+PrRows* pr_layout(gbg_graph* g);
+uint64_t pagerank_rows_run(gbg_graph* g, double damping, uint64_t max_iters, double tol, double* p_dev);
+double rows_build_ms(const PrRows* L);
+}  // namespace prrows
 
 // Optional phase timing (environment GBG_TRACE=1): CUDA events on the
 // handle's stream at named points, device-time deltas printed to stderr

@@ -25,16 +25,16 @@
 // HBM roofline).  The index instead
 //   * renumbers vertices by (degree desc, id asc), so the gathered vector's
 //     hot part is contiguous and rows of similar degree are adjacent;
-//   * cuts the rows with edges into blocks of kRows = 16384 consecutive
+//   * cuts the rows with edges into blocks of kRows = 8192 consecutive
 //     rows, and sorts each block's arcs by SOURCE (the gathered vertex):
 //     one warp load then reads 32 consecutive arcs whose sources share a
-//     few 128-byte lines (scale 24: 0.094 line requests per arc instead of
+//     few 128-byte lines (scale 24: ~0.1 line requests per arc instead of
 //     ~1.03 sectors), and an arc of a hub source becomes part of a "run" of
-//     equal sources (0.22 runs per arc);
-//   * stores per arc only its row inside the block (14 bits) and a run-start
-//     bit, in 16 bits, plus one uint32 source id per run: 2.9 B per arc
+//     equal sources (~0.25 runs per arc);
+//   * stores per arc only its row inside the block (13 bits) and a run-start
+//     bit, in 16 bits, plus one uint32 source id per run: ~3 B per arc
 //     against 4 B of neighbour id in the CSR;
-//   * accumulates each block's row sums in shared memory (128 KiB per CTA)
+//   * accumulates each block's row sums in shared memory (64 KiB per CTA)
 //     as 64-bit fixed point (2^-62 units): integer atomics are
 //     order-independent, so the result is deterministic whatever the
 //     schedule, and the rounding (<= 2^-63 per term) stays ~1e-12 in
@@ -62,14 +62,18 @@
 namespace gbg {
 
 #ifndef GBG_PR_ROW_BITS
-#define GBG_PR_ROW_BITS 14
+#define GBG_PR_ROW_BITS 13
 #endif
 constexpr int kRowBits = GBG_PR_ROW_BITS;
 constexpr uint32_t kRows = 1u << kRowBits;  // rows per block: 8 B of fixed-point sum each in shared memory
 constexpr uint16_t kRunStart = 0x8000;      // arc word: run-start bit | row in block
 constexpr uint32_t kGroup = 256;            // arcs per warp work item (8 rounds of 32)
 constexpr int kConsumers = 31;              // consumer warps; warp 31 issues the bulk copies
-constexpr uint32_t kChunkGroups = kConsumers;  // groups per staged chunk at most: one per consumer warp
+#ifndef GBG_PR_WARP_GROUPS
+#define GBG_PR_WARP_GROUPS 2
+#endif
+constexpr uint32_t kWarpGroups = GBG_PR_WARP_GROUPS;            // groups per consumer warp per chunk
+constexpr uint32_t kChunkGroups = kConsumers * kWarpGroups;     // groups per staged chunk at most
 constexpr uint32_t kChunk = kChunkGroups * kGroup;
 #ifndef GBG_PR_RUN_BUF
 #define GBG_PR_RUN_BUF 4096
@@ -81,12 +85,7 @@ constexpr uint32_t kRunBuf = GBG_PR_RUN_BUF + 8;  // staged runs per chunk at mo
 constexpr uint32_t kArcBuf = kChunk + 16;   // staged arc words (u16, + 16-byte alignment slack)
 constexpr uint32_t kGrpBuf = (kChunkGroups + 8 + 3) & ~3u;  // staged group run bases (u32)
 constexpr int kStages = GBG_PR_STAGES;
-#ifndef GBG_PR_PREFETCH
-#define GBG_PR_PREFETCH 0
-#endif
-#ifndef GBG_PR_EXPERIMENT
-#define GBG_PR_EXPERIMENT 0
-#endif      // shared-memory ring depth
+      // shared-memory ring depth
 #ifndef GBG_PR_TILE_ARCS
 #define GBG_PR_TILE_ARCS (1u << 17)
 #endif
@@ -627,18 +626,6 @@ struct StageInfo {
   uint32_t valid;
 };
 
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return done != 0;
-}
-__device__ __forceinline__ void prefetch_l2_last(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -692,19 +679,8 @@ __device__ __forceinline__ void pr_group(const PrArgs& a, uint32_t* lo, uint32_t
     const uint32_t run = rbase + __popc(flags[j] & le);
     rbase += __popc(flags[j]);
     const uint32_t u = srun[run];
-#if GBG_PR_EXPERIMENT == 2
-    x[j] = on[j] ? u : 0ull;
-#else
     x[j] = on[j] ? ld_fix(a.t_old + u, u < kHot ? pl : pf) : 0ull;
-#endif
   }
-#if GBG_PR_EXPERIMENT == 1
-  unsigned long long t = 0;
-#pragma unroll
-  for (int j = 0; j < R; ++j) t += x[j] + row[j];
-  if (t == 12345) lo[lane] = 1;
-  return;
-#endif
   uint32_t old[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) old[j] = on[j] ? atomicAdd(lo + row[j], static_cast<uint32_t>(x[j])) : 0u;
@@ -833,36 +809,12 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
         consumer_sync();
       }
       {
-        // L2 prefetch of the contribs the same warp gathers in the next
-        // chunk (if it has landed): one prefetch per run of that group, so
-        // the group after this one finds its cold sources in L2
-        const int s1 = (c + 1) % kStages;
-        if (GBG_PR_PREFETCH && mbar_test(&s_full[s1], ((c + 1) / kStages) & 1) && s_stage[s1].valid) {
-          const PrChunk n1 = s_stage[s1].ch;
-          const uint32_t ng1 = n1.flags & 0xff;
-          if (warp < ng1) {
-            uint16_t* arcb1;
-            uint32_t* runb1;
-            uint32_t* grpb1;
-            stage_ptrs(s1, arcb1, runb1, grpb1);
-            const uint32_t q1 = s_stage[s1].qbase;
-            const uint32_t r0 = grpb1[n1.g0 + warp - q1] - n1.rlo;  // may wrap to ~0u: run 0 covered below
-            const uint32_t r1 = warp + 1 < ng1 ? grpb1[n1.g0 + warp + 1 - q1] - n1.rlo : n1.rhi - n1.rlo - 1;
-            for (uint32_t r = r0 + lane; static_cast<int32_t>(r - r1) <= 0; r += 32) {
-              const uint32_t u = runb1[r == ~0u ? 0u : r];
-              prefetch_l2_last(a.t_old + u);
-            }
-          }
-        }
-      }
-      {
         uint16_t* arcb;
         uint32_t* runb;
         uint32_t* grpb;
         stage_ptrs(s, arcb, runb, grpb);
         const uint32_t ng = ch.flags & 0xff;
-        if (warp < ng) {  // consumer warp w takes the chunk's group w
-          const uint32_t gi = warp;
+        for (uint32_t gi = warp; gi < ng; gi += kConsumers) {  // warp w: groups w, w + 31, ...
           const uint32_t off = gi * kGroup;
           const uint32_t len = min(kGroup, ch.len - off);
           const uint32_t rb = grpb[ch.g0 + gi - qbase];
@@ -883,7 +835,8 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
         const uint32_t b = ch.block;
         if (!(ch.flags & (1u << 10))) {
           // the whole block in this tile: finalize from shared memory
-          for (uint32_t i = ctid; i < nrows; i += kCT) pr_finalize(a, base, row0 + i, acc_get(s_lo, s_hi, i), err, pf, pl);
+          for (uint32_t i = ctid; i < nrows; i += kCT)
+            pr_finalize(a, base, row0 + i, acc_get(s_lo, s_hi, i), err, pf, pl);
           fin = true;
         } else {
           for (uint32_t i = ctid; i < nrows; i += kCT) {
@@ -1004,27 +957,6 @@ PrLayout* pr_layout(gbg_graph* g) {
   return g->pr;
 }
 
-// pipelined CSR builds (api.cu)
-PrLayout* pr_layout_rows_csr(gbg_graph* g) { return layout_rows(g, g->csr_view()); }
-void pr_layout_relabel_csr(gbg_graph* g, PrLayout* L, uint64_t e0, uint64_t e1) {
-  layout_keys(g, g->csr_view(), g->off, L, e0, e1);
-}
-void pr_layout_attach(gbg_graph* g, PrLayout* L, float build_ms) {
-  cudaEvent_t e0, e1;
-  GBG_CUDA(cudaEventCreate(&e0));
-  GBG_CUDA(cudaEventCreate(&e1));
-  GBG_CUDA(cudaEventRecord(e0, g->stream));
-  layout_finish(g, L);
-  GBG_CUDA(cudaEventRecord(e1, g->stream));
-  GBG_CUDA(cudaEventSynchronize(e1));
-  float ms = 0;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  L->build_ms = build_ms + ms;
-  g->pr = L;
-}
-void pr_layout_free(PrLayout* L) { delete L; }
 uint64_t pr_layout_bytes(const PrLayout* L) { return L ? L->bytes() : 0; }
 
 uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double tol, double* p_dev) {
@@ -1085,6 +1017,8 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
 void gbg_graph::invalidate_derived() {
   delete pr;
   pr = nullptr;
+  if (pr_rows) gbg::prrows::pr_layout_free(pr_rows);
+  pr_rows = nullptr;
   voff_valid = false;
   first_valid = false;
 }
@@ -1110,8 +1044,10 @@ gbg_status pagerank_entry(gbg_graph* g, double damping, uint64_t max_iters, doub
       // no iteration: p = 1/n (algorithms.cpp:520)
       std::vector<double> init(g->n, 1.0 / static_cast<double>(g->n));
       GBG_CUDA(cudaMemcpyAsync(p, init.data(), g->n * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+    } else if (g->pr) {
+      done = pagerank_run(g, damping, max_iters, tol, p);  // tiled index (prepared)
     } else {
-      done = pagerank_run(g, damping, max_iters, tol, p);
+      done = prrows::pagerank_rows_run(g, damping, max_iters, tol, p);  // one-shot row path
     }
     if (host) GBG_CUDA(cudaMemcpyAsync(out, p, g->n * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
     GBG_CUDA(cudaStreamSynchronize(g->stream));

@@ -28,3 +28,15 @@ def complete(n):
 
 def members(mask):
     return set(np.nonzero(np.asarray(mask))[0].tolist())
+
+
+PR_PATHS = ["rows", "tiled"]
+
+
+def pagerank_on(gbg, g, path, *args):
+    """gbg.pagerank through one of the two device paths: "rows" (the
+    one-shot path a fresh container uses) or "tiled" (the source-sorted
+    index gbg_pagerank_prepare builds, used by every later call)."""
+    if path == "tiled":
+        gbg.pagerank_prepare(g)
+    return gbg.pagerank(g, *args)

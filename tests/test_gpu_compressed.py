@@ -101,6 +101,9 @@ def test_rmat_compressed_algorithms_match_golden(gbg, S):
     ids = np.array(gd["pagerank"]["sample_ids"])
     want = np.array([float.fromhex(h) for h in gd["pagerank"]["sample_hex"]])
     assert float(np.abs(p[ids] - want).sum() / np.abs(want).sum()) <= 1e-9
+    gbg.pagerank_prepare(z)  # the tiled index path on the compressed container
+    p = gbg.pagerank(z, 0.85, 20, TINY)
+    assert float(np.abs(p[ids] - want).sum() / np.abs(want).sum()) <= 1e-9
     with gbg.CsrGraph.from_csr(off, nbr) as c:
         assert np.array_equal(gbg.bc(z, 0), gbg.bc(c, 0))
 

@@ -5,7 +5,7 @@ degenerate update batches.  Everything is compared with the C oracle."""
 import numpy as np
 import pytest
 
-from tests.helpers import csr, undirected
+from tests.helpers import PR_PATHS, csr, pagerank_on, undirected
 
 pytestmark = pytest.mark.gpu
 TINY = np.finfo(np.float64).tiny
@@ -15,23 +15,25 @@ def rel_l1(a, b):
     return float(np.abs(a - b).sum() / max(np.abs(b).sum(), 1e-300))
 
 
+@pytest.mark.parametrize("path", PR_PATHS)
 @pytest.mark.parametrize("kind", ["csr", "blocked"])
-def test_empty_and_singleton_graphs(gbg, kind):
+def test_empty_and_singleton_graphs(gbg, kind, path):
     mk = gbg.CsrGraph.build if kind == "csr" else gbg.BlockedGraph.build
     g0 = mk(0, [])
     assert g0.num_vertices() == 0 and g0.num_edges() == 0
-    assert gbg.pagerank(g0).size == 0 and gbg.cc(g0).size == 0
+    assert pagerank_on(gbg, g0, path).size == 0 and gbg.cc(g0).size == 0
     with pytest.raises(IndexError):
         gbg.bfs(g0, 0)
     g1 = mk(1, [])
     assert gbg.bfs(g1, 0).depth.tolist() == [0]
     assert gbg.cc(g1).tolist() == [0]
-    assert np.allclose(gbg.pagerank(g1, 0.85, 20, TINY), [1.0])
+    assert np.allclose(pagerank_on(gbg, g1, path, 0.85, 20, TINY), [1.0])
     assert gbg.triangle_count(g1) == 0
 
 
+@pytest.mark.parametrize("path", PR_PATHS)
 @pytest.mark.parametrize("kind", ["csr", "blocked"])
-def test_deep_path_bfs(gbg, orc, kind):
+def test_deep_path_bfs(gbg, orc, kind, path):
     """A 3000-vertex path: 2999 levels, far beyond GBG_MAX_LEVELS."""
     n = 3000
     nn, pairs = undirected(n, [(i, i + 1) for i in range(n - 1)], orc)
@@ -45,10 +47,11 @@ def test_deep_path_bfs(gbg, orc, kind):
         k = min(len(modes), 64)
         assert r.modes[:k] == modes[:k] and r.frontier_sizes[:k] == sizes[:k]
     assert gbg.cc(g).tolist() == [0] * n
-    assert rel_l1(gbg.pagerank(g, 0.85, 20, TINY), orc.pagerank(nn, off, nbr, 0.85, 20, TINY)) <= 1e-9
+    assert rel_l1(pagerank_on(gbg, g, path, 0.85, 20, TINY), orc.pagerank(nn, off, nbr, 0.85, 20, TINY)) <= 1e-9
 
 
-def test_huge_star_and_disconnected_pieces(gbg, orc):
+@pytest.mark.parametrize("path", PR_PATHS)
+def test_huge_star_and_disconnected_pieces(gbg, orc, path):
     """One hub of 200k leaves (far above every split threshold) plus a
     triangle and isolated vertices."""
     leaves = 200_000
@@ -62,19 +65,20 @@ def test_huge_star_and_disconnected_pieces(gbg, orc):
         assert np.array_equal(gbg.bfs(g, src).depth, orc.bfs(nn, off, nbr, src)[0])
     assert np.array_equal(gbg.cc(g), orc.cc(nn, off, nbr))
     assert gbg.triangle_count(g) == 1
-    assert rel_l1(gbg.pagerank(g, 0.85, 20, TINY), orc.pagerank(nn, off, nbr, 0.85, 20, TINY)) <= 1e-9
+    assert rel_l1(pagerank_on(gbg, g, path, 0.85, 20, TINY), orc.pagerank(nn, off, nbr, 0.85, 20, TINY)) <= 1e-9
     # early convergence: the tolerance break (algorithms.cpp:552)
     for tol in (1e-3, 1e-6):
-        assert rel_l1(gbg.pagerank(g, 0.85, 100, tol), orc.pagerank(nn, off, nbr, 0.85, 100, tol)) <= 1e-9
+        assert rel_l1(pagerank_on(gbg, g, path, 0.85, 100, tol), orc.pagerank(nn, off, nbr, 0.85, 100, tol)) <= 1e-9
 
 
-def test_complete_graph(gbg, orc):
+@pytest.mark.parametrize("path", PR_PATHS)
+def test_complete_graph(gbg, orc, path):
     k = 300
     nn, pairs = undirected(k, [(i, j) for i in range(k) for j in range(i + 1, k)], orc)
     g = gbg.CsrGraph.build(nn, pairs)
     d = gbg.bfs(g, 7).depth
     assert d[7] == 0 and set(d.tolist()) == {0, 1}
-    assert np.allclose(gbg.pagerank(g, 0.85, 20, TINY), 1.0 / k, rtol=1e-12, atol=0)
+    assert np.allclose(pagerank_on(gbg, g, path, 0.85, 20, TINY), 1.0 / k, rtol=1e-12, atol=0)
     assert gbg.triangle_count(g) == k * (k - 1) * (k - 2) // 6
 
 

@@ -11,7 +11,7 @@ import pytest
 
 from oracle.bindings import RMAT_A, RMAT_B, RMAT_C, digest, max_degree_source
 from tests.conftest import golden
-from tests.helpers import T4_PAIRS, complete, csr, members, star, undirected
+from tests.helpers import PR_PATHS, pagerank_on, T4_PAIRS, complete, csr, members, star, undirected
 
 pytestmark = pytest.mark.gpu
 TINY = np.finfo(np.float64).tiny
@@ -291,7 +291,8 @@ def test_scale24_bfs_cc_match_golden(gbg):
     assert abs(p.sum() - gd["pagerank"]["sum"]) <= PR_TOL
 
 
-def test_scale24_pagerank_full_vector_matches_reference(gbg, ref):
+@pytest.mark.parametrize("path", PR_PATHS)
+def test_scale24_pagerank_full_vector_matches_reference(gbg, ref, path):
     """The headline config at the BASELINE bar: all 16.8M ranks of the
     device PageRank against the reference library's own
     gb::pagerank(view, 0.85, 20, DBL_MIN) (algorithms.cpp:508-555) on the
@@ -305,7 +306,7 @@ def test_scale24_pagerank_full_vector_matches_reference(gbg, ref):
     ref.set_threads(os.cpu_count() or 1)
     want = ref.csr(n, off, nbr).pagerank(0.85, 20, TINY)
     del off, nbr
-    got = gbg.pagerank(g, 0.85, 20, TINY)
+    got = pagerank_on(gbg, g, path, 0.85, 20, TINY)
     assert got.shape == want.shape == (n,)
     err = rel_l1(got, want)
     assert err <= PR_TOL, err
@@ -327,42 +328,46 @@ def test_pagerank_known_answers(gbg, orc):
         gbg.pagerank(g, 0.85, 20, 0.0)
 
 
+@pytest.mark.parametrize("path", PR_PATHS)
 @pytest.mark.parametrize("kind", ["csr", "blocked"])
-def test_pagerank_matches_oracle_seeded(gbg, ref, orc, kind):
+def test_pagerank_matches_oracle_seeded(gbg, ref, orc, kind, path):
     for trial in range(15):
         n, pairs = ref.er(150 + 101 * trial, 0.04, 2300 + trial)
         off, nbr = csr(n, pairs)
         g = gbg.CsrGraph.build(n, pairs) if kind == "csr" else gbg.BlockedGraph.build(n, pairs)
         for tol in (1e-4, TINY):
             want = orc.pagerank(n, off, nbr, 0.85, 20, tol)
-            got = gbg.pagerank(g, 0.85, 20, tol)
+            got = pagerank_on(gbg, g, path, 0.85, 20, tol)
             assert rel_l1(got, want) <= PR_TOL, (trial, tol)
 
 
+@pytest.mark.parametrize("path", PR_PATHS)
 @pytest.mark.parametrize("S", [16, 20])
-def test_pagerank_rmat_matches_reference(gbg, ref, S):
+def test_pagerank_rmat_matches_reference(gbg, ref, S, path):
     gd = golden(S)
     g = gbg.generate_rmat(S, 16 << S, 1, RMAT_A, RMAT_B, RMAT_C)
     off, nbr = g.to_csr()
     want = ref.csr(gd["n"], off, nbr).pagerank(0.85, 20, TINY)
-    got = gbg.pagerank(g, 0.85, 20, TINY)
+    got = pagerank_on(gbg, g, path, 0.85, 20, TINY)
     assert rel_l1(got, want) <= PR_TOL
     ids = np.array(gd["pagerank"]["sample_ids"])
     gold = np.array([float.fromhex(h) for h in gd["pagerank"]["sample_hex"]])
     assert rel_l1(got[ids], gold) <= PR_TOL
 
 
-def test_pagerank_hub_rows(gbg, orc):
+@pytest.mark.parametrize("path", PR_PATHS)
+def test_pagerank_hub_rows(gbg, orc, path):
     # rows far above the heavy-row split (kHeavy) and many straddling tiles
     edges = [(0, v) for v in range(1, 20000)] + [(1, v) for v in range(2, 9000, 3)] + complete(60)
     n, pairs = undirected(20001, edges, orc)
     off, nbr = csr(n, pairs)
-    got = gbg.pagerank(gbg.CsrGraph.build(n, pairs), 0.85, 20, TINY)
+    got = pagerank_on(gbg, gbg.CsrGraph.build(n, pairs), path, 0.85, 20, TINY)
     want = orc.pagerank(n, off, nbr, 0.85, 20, TINY)
     assert rel_l1(got, want) <= PR_TOL
 
 
-def test_pagerank_asymmetric_arcs(gbg, orc):
+@pytest.mark.parametrize("path", PR_PATHS)
+def test_pagerank_asymmetric_arcs(gbg, orc, path):
     """Directed arc sets: vertices with in-arcs but no out-arcs are dangling
     (contrib 0, mass redistributed) yet gathered by their in-neighbours, on
     both containers, with early stopping and with 20 fixed iterations."""
@@ -376,7 +381,7 @@ def test_pagerank_asymmetric_arcs(gbg, orc):
         for g in (gbg.CsrGraph.build(n, pairs), gbg.BlockedGraph.build(n, pairs)):
             for tol in (1e-4, TINY):
                 want = orc.pagerank(n, off, nbr, 0.85, 20, tol)
-                assert rel_l1(gbg.pagerank(g, 0.85, 20, tol), want) <= PR_TOL, (trial, tol)
+                assert rel_l1(pagerank_on(gbg, g, path, 0.85, 20, tol), want) <= PR_TOL, (trial, tol)
 
 
 # ---------------------------------------------------------------- CC / TC
@@ -468,6 +473,29 @@ def test_blocked_t4_apply_counts(gbg):
     with pytest.raises(ValueError):
         g.insert_edge(1, 1)
     assert g.insert_edge(0, 1) and not g.insert_edge(0, 1) and g.delete_edge(0, 1)
+
+
+@pytest.mark.parametrize("path", PR_PATHS)
+def test_pagerank_after_batches_on_blocked_container(gbg, ref, path):
+    """PageRank on the dynamic container after insert and delete batches:
+    both derived PageRank layouts are dropped by an update and rebuilt on
+    the next call, so every call matches gb::pagerank on the container's
+    current arcs (asymmetric batches included)."""
+    n, base = ref.rmat(14, 16 << 14, 5, RMAT_A, RMAT_B, RMAT_C)
+    g = gbg.BlockedGraph.build(n, base)
+    rng = np.random.default_rng(3)
+    for step in range(4):
+        pagerank_on(gbg, g, path, 0.85, 20, TINY)  # layouts exist before the update
+        raw = ref.update_batch(14, 3000, 77 + step, RMAT_A, RMAT_B, RMAT_C)
+        if step == 2:
+            raw = rng.integers(0, n, size=(500, 2)).astype(np.uint32)  # one-directional arcs
+        if step == 3:
+            g.delete_batch(raw)
+        else:
+            g.insert_batch(raw)
+        off, nbr = g.to_csr()
+        want = ref.csr(n, off, nbr).pagerank(0.85, 20, TINY)
+        assert rel_l1(pagerank_on(gbg, g, path, 0.85, 20, TINY), want) <= PR_TOL, step
 
 
 def test_blocked_churn_matches_oracle(gbg, ref, orc):
