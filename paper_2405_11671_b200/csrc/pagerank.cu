@@ -305,7 +305,9 @@ struct TileOut {
 struct GroupsIn {
   const uint64_t* tile_arc;
   __device__ __forceinline__ uint32_t operator()(uint64_t t) const {
-    return static_cast<uint32_t>((tile_arc[t + 1] - tile_arc[t] + kGroup - 1) / kGroup);
+    // groups are 256-arc windows aligned to the tile's first arc rounded
+    // down to 8 (16-byte shared-memory loads), clipped to the tile
+    return static_cast<uint32_t>((tile_arc[t + 1] - (tile_arc[t] & ~uint64_t{7}) + kGroup - 1) / kGroup);
   }
 };
 
@@ -333,7 +335,7 @@ struct GroupBaseOp {
   uint64_t nruns;
   uint32_t* grp_rbase;
   __device__ __forceinline__ void operator()(uint32_t t, uint32_t rank, uint64_t flat) const {
-    const uint64_t e0 = tile_arc[t] + static_cast<uint64_t>(rank) * kGroup;
+    const uint64_t e0 = max(tile_arc[t], (tile_arc[t] & ~uint64_t{7}) + static_cast<uint64_t>(rank) * kGroup);
     uint64_t lo = 0, hi = nruns;
     while (lo < hi) {
       const uint64_t mid = (lo + hi) >> 1;
@@ -366,8 +368,9 @@ __global__ void chunk_cut_k(const uint64_t* tile_arc, const uint32_t* tile_grp, 
       while (g1 < gb && g1 - g0 < kChunkGroups && run_hi(grp_rbase[g1 + 1]) - rlo <= kRunBuf) ++g1;
       if (kFill) {
         PrChunk ch;
-        ch.e0 = tb + static_cast<uint64_t>(g0 - ga) * kGroup;
-        const uint64_t e1 = g1 == gb ? te : tb + static_cast<uint64_t>(g1 - ga) * kGroup;
+        const uint64_t ta = tb & ~uint64_t{7};
+        ch.e0 = max(tb, ta + static_cast<uint64_t>(g0 - ga) * kGroup);
+        const uint64_t e1 = g1 == gb ? te : ta + static_cast<uint64_t>(g1 - ga) * kGroup;
         ch.len = static_cast<uint32_t>(e1 - ch.e0);
         ch.g0 = g0;
         ch.rlo = rlo;
@@ -545,9 +548,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
         : "memory");
   } while (!done);
 }
@@ -562,6 +565,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ unsigned long long ld_fix(const unsigned long long* a, uint64_t pol) {
   unsigned long long v;
   asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
+// predicated gather (0 when !p) in one asm block, so the compiler cannot
+// fold the later register select into the load's destination (which would
+// chain the loads one after the other)
+__device__ __forceinline__ unsigned long long ld_fix_if(const unsigned long long* a, uint64_t pol, uint32_t p) {
+  unsigned long long v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n mov.b64 %0, 0;\n"
+      " @q ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;\n}"
+      : "=l"(v)
+      : "l"(a), "l"(pol), "r"(p));
   return v;
 }
 
@@ -649,46 +665,61 @@ __device__ __forceinline__ double consumer_sum(double v, double* red) {
   return r;
 }
 
-// One work group: n (<= kGroup) arcs of the staged chunk, as 8 rounds of 32
-// consecutive arcs.  A round's run starts are ballot-ranked onto the run
-// index carried from the group's base, so every lane finds its arc's source
-// in the staged runs; lanes of one run gather the same contrib (one
-// request), and consecutive runs have consecutive sources.  All 8 gathers
-// are in flight before the first add; then the 8 low-word adds (with
-// return), then the 8 high-word adds (carry + high half; no return).
-// kFull: n == kGroup (every group but a tile's last), no bounds checks.
+// high word += high half of the term + carry out of the low word's add
+// (old = the low word before the add)
+__device__ __forceinline__ uint32_t carry_hi(uint32_t old, uint32_t l, uint32_t h) {
+  uint32_t c;
+  asm("{\n .reg .u32 t;\n add.cc.u32 t, %1, %2;\n addc.u32 %0, %3, 0;\n}" : "=r"(c) : "r"(old), "r"(l), "r"(h));
+  return c;
+}
+
+// One work group: a 256-arc window of the staged chunk, arcs [vlo, vhi) of
+// it valid (kFull: all), as 8 rounds of 32 consecutive arcs.  A round's
+// run starts are ballot-ranked onto the run index carried from the group's
+// base, so every lane finds its arc's source in the staged runs; lanes of
+// one run gather the same contrib (one request), and consecutive runs have
+// consecutive sources.  All 8 gathers are in flight before the first add;
+// then the 8 low-word adds (with return), then the 8 high-word adds (high
+// half + carry; no return).
 template <bool kFull>
-__device__ __forceinline__ void pr_group(const PrArgs& a, uint32_t* lo, uint32_t* hi, const uint16_t* sarc,
-                                         const uint32_t* srun, uint32_t n, uint32_t rbase, uint32_t lane,
-                                         uint64_t pf, uint64_t pl) {
+__device__ __forceinline__ void pr_group(const PrArgs& a, uint32_t* lo, uint32_t* hi, const uint16_t* win,
+                                         const uint32_t* srun, uint32_t vlo, uint32_t vhi, uint32_t rbase,
+                                         uint32_t lane, uint64_t pf, uint64_t pl) {
   constexpr int R = kGroup / 32;
   uint32_t row[R];
   bool on[R];
   uint32_t flags[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    on[j] = kFull || j * 32 + lane < n;
-    const uint32_t w = on[j] ? sarc[j * 32 + lane] : 0u;
+    const uint32_t i = j * 32 + lane;
+    on[j] = kFull || (i >= vlo && i < vhi);
+    const uint32_t w = on[j] ? win[i] : 0u;
     row[j] = w & (kRows - 1);
     flags[j] = __ballot_sync(0xffffffffu, (w & kRunStart) != 0);
   }
   const uint32_t le = (2u << lane) - 1u;  // lanes <= this one
+  // one L2 policy for the whole group: sources ascend inside a block, so
+  // the group's last run decides (evict_last when it is hot; a group that
+  // straddles kHot is rare)
+  uint32_t rend = rbase;
+#pragma unroll
+  for (int j = 0; j < R; ++j) rend += __popc(flags[j]);
+  const uint64_t pol = srun[rend] < kHot ? pl : pf;
   unsigned long long x[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const uint32_t run = rbase + __popc(flags[j] & le);
     rbase += __popc(flags[j]);
     const uint32_t u = srun[run];
-    x[j] = on[j] ? ld_fix(a.t_old + u, u < kHot ? pl : pf) : 0ull;
+    x[j] = on[j] ? ld_fix(a.t_old + u, pol) : 0ull;
   }
   uint32_t old[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) old[j] = on[j] ? atomicAdd(lo + row[j], static_cast<uint32_t>(x[j])) : 0u;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const uint32_t l = static_cast<uint32_t>(x[j]);
-    const uint32_t c = static_cast<uint32_t>(x[j] >> 32) + (old[j] + l < old[j] ? 1u : 0u);
-    if (on[j] && c) atomicAdd(hi + row[j], c);  // lanes with nothing to carry stay idle
+    const uint32_t c = carry_hi(old[j], static_cast<uint32_t>(x[j]), static_cast<uint32_t>(x[j] >> 32));
+    if (kFull || on[j]) atomicAdd(hi + row[j], c);  // result unused: RED (adds 0 when nothing carries)
   }
 }
 
@@ -795,6 +826,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
     const double base = (1.0 - a.damping) / a.nd + a.damping * dcur / a.nd;
     const uint32_t ctid = threadIdx.x;  // < kConsumers * 32
     constexpr uint32_t kCT = kConsumers * 32;
+    uint32_t rot = 0;
     for (uint32_t c = 0;; ++c) {
       const int s = c % kStages;
       mbar_wait(&s_full[s], (c / kStages) & 1);
@@ -814,17 +846,24 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
         uint32_t* grpb;
         stage_ptrs(s, arcb, runb, grpb);
         const uint32_t ng = ch.flags & 0xff;
-        for (uint32_t gi = warp; gi < ng; gi += kConsumers) {  // warp w: groups w, w + 31, ...
+        // group gi goes to warp (rot + gi) mod 31: the assignment rotates
+        // from chunk to chunk, so no warp takes the extra group of every
+        // chunk (a chunk's group count is rarely a multiple of 31)
+        // group gi = the 256-arc window at staged arc gi * 256 (the stage
+        // starts at ch.e0 rounded down to 8), valid arcs [v0, v1) of it
+        const uint32_t v0 = static_cast<uint32_t>(ch.e0 - abase), v1 = v0 + ch.len;
+        for (uint32_t gi = (warp + kConsumers - rot) % kConsumers; gi < ng; gi += kConsumers) {
           const uint32_t off = gi * kGroup;
-          const uint32_t len = min(kGroup, ch.len - off);
+          const uint32_t vlo = gi == 0 ? v0 : 0u, vhi = min(kGroup, v1 - off);
           const uint32_t rb = grpb[ch.g0 + gi - qbase];
-          const uint16_t* sa = arcb + static_cast<uint32_t>(ch.e0 - abase) + off;
           // staged run index = global run index - rlo (rb may be ~0u: wraps consistently)
-          if (len == kGroup)
-            pr_group<true>(a, s_lo, s_hi, sa, runb, len, rb - ch.rlo, lane, pf, pl);
+          const uint32_t rs = rb - ch.rlo;
+          if (vlo == 0 && vhi == kGroup)
+            pr_group<true>(a, s_lo, s_hi, arcb + off, runb, 0, kGroup, rs, lane, pf, pl);
           else
-            pr_group<false>(a, s_lo, s_hi, sa, runb, len, rb - ch.rlo, lane, pf, pl);
+            pr_group<false>(a, s_lo, s_hi, arcb + off, runb, vlo, vhi, rs, lane, pf, pl);
         }
+        rot = (rot + ng) % kConsumers;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[s]);
