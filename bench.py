@@ -242,6 +242,11 @@ def run_bfs(torch, gbg, g, src, steps, warmup):
     for _ in range(warmup):
         step()
     t = events_time(torch, g.stream(), step, steps)
+    # per-level device timestamps from one extra, untimed call (the timed
+    # path carries no instrumentation)
+    os.environ["GBG_BFS_LEVEL_TIMES"] = "1"
+    step()
+    os.environ.pop("GBG_BFS_LEVEL_TIMES")
     return t / steps, stats, depth
 
 

@@ -77,7 +77,7 @@ typedef struct gbg_bfs_stats {
   uint64_t frontier[GBG_MAX_LEVELS];     /* |F| fed to level i             */
   uint64_t degree_sum[GBG_MAX_LEVELS];   /* sum deg(F) fed to level i      */
   uint64_t reached;                      /* vertices with depth >= 0       */
-  float level_ms[GBG_MAX_LEVELS];        /* device time of level i (events) */
+  float level_ms[GBG_MAX_LEVELS];        /* device time of level i; persistent path: only with GBG_BFS_LEVEL_TIMES=1, else 0 */
   uint64_t examined[GBG_MAX_LEVELS];     /* arcs inspected by level i in the reference's
                                             order: sum deg(F) for a push, and for an
                                             early-exit pull each vertex's list up to

@@ -112,6 +112,7 @@ struct CoopState {
   unsigned long long* level_examined;  // [GBG_MAX_LEVELS] arcs inspected by dense levels
   unsigned* level_heavy;       // [GBG_MAX_LEVELS] a dense level reached a vertex of degree > kBitmapPushMaxDeg
   int bitmap_push;             // dense -> sparse transitions push straight from the bitmap
+  int timing;                  // record level_ns (GBG_BFS_LEVEL_TIMES=1; diagnostics only)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kPushThreads, GBG_BFS_MINB) bfs_coop_k(G g, Co
   if (tid == 0) {
     s.list[0][0] = s.src;
     s.dscan[0][0] = 0;
-    s.level_ns[0] = globaltimer();
+    if (s.timing) s.level_ns[0] = globaltimer();
   }
   grid.sync();
   int cur = 0;      // list buffers
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kPushThreads, GBG_BFS_MINB) bfs_coop_k(G g, Co
       }
     }
     grid.sync();
-    if (tid == 0 && level <= GBG_MAX_LEVELS) s.level_ns[level] = globaltimer();
+    if (s.timing && tid == 0 && level <= GBG_MAX_LEVELS) s.level_ns[level] = globaltimer();
     cur = nxt;
     bcur = bnxt;
   }
@@ -357,6 +358,14 @@ bool bitmap_push_enabled() {
 }
 
 // The persistent path; false when the device cannot co-schedule the grid.
+// per-level device timestamps in the persistent kernel: off unless
+// GBG_BFS_LEVEL_TIMES=1 (read per call), so the timed path carries no
+// instrumentation; gbg_bfs_stats.level_ms is 0 when off
+bool level_times_enabled() {
+  const char* v = std::getenv("GBG_BFS_LEVEL_TIMES");
+  return v && v[0] == '1';
+}
+
 template <class G>
 bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats* st) {
   if (!coop_enabled(g->device)) return false;
@@ -399,6 +408,7 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   s.level_mode = reinterpret_cast<int32_t*>(stat + 3 * ML + 4);
   s.level_heavy = g->ws.get<unsigned>("bfs.heavy", ML);
   s.bitmap_push = bitmap_push_enabled();
+  s.timing = level_times_enabled();
   s.blocksum = g->ws.get<uint64_t>("bfs.blocksum", grid);
   s.nw = tb.nw;
   s.threshold = (1.0 / 20.0) * static_cast<double>(g->m);
@@ -423,7 +433,8 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
       st->mode[i] = hm[i];
       st->frontier[i] = pack_count(hs[i]);
       st->degree_sum[i] = pack_degsum(hs[i]);
-      st->level_ms[i] = static_cast<float>((hs[GBG_MAX_LEVELS + i + 1] - hs[GBG_MAX_LEVELS + i]) * 1e-6);
+      st->level_ms[i] =
+          s.timing ? static_cast<float>((hs[GBG_MAX_LEVELS + i + 1] - hs[GBG_MAX_LEVELS + i]) * 1e-6) : 0.0f;
       st->examined[i] = hm[i] == GBG_MODE_DENSE ? hx[i] : st->degree_sum[i];
     }
   }
