@@ -71,14 +71,19 @@ __device__ __forceinline__ T block_sum(T v, T* smem) {
   return r;
 }
 
+// Tile t covers items [t * kScanTile, (t + 1) * kScanTile).  Loads are
+// warp-striped: warp w owns the 512 consecutive items from t * kScanTile +
+// w * 512, read as 16 rounds of 32 consecutive items (one coalesced load per
+// round), so the input functors (which often read neighbouring elements)
+// touch each sector once.
 template <class T, class In>
 __global__ void __launch_bounds__(kScanThreads) scan_reduce_k(In in, uint64_t count, T* sums) {
   __shared__ T sm[33];
-  uint64_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  const uint64_t base = blockIdx.x * kScanTile + threadIdx.x;
   T acc = 0;
 #pragma unroll 4
   for (int j = 0; j < kScanItems; ++j)
-    if (base + j < count) acc += in(base + j);
+    if (base + j * kScanThreads < count) acc += in(base + j * kScanThreads);
   T t = block_sum<T>(acc, sm);
   if (threadIdx.x == 0) sums[blockIdx.x] = t;
 }
@@ -103,20 +108,27 @@ __global__ void __launch_bounds__(1024) scan_sums_k(T* sums, uint64_t nb, T* tot
 template <class T, class In, class Out>
 __global__ void __launch_bounds__(kScanThreads) scan_down_k(In in, Out out, uint64_t count, const T* sums) {
   __shared__ T sm[33];
-  uint64_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t sub = blockIdx.x * kScanTile + static_cast<uint64_t>(warp) * (32 * kScanItems);
   T vals[kScanItems];
   T acc = 0;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    vals[j] = base + j < count ? in(base + j) : T(0);
+    const uint64_t i = sub + j * 32 + lane;
+    vals[j] = i < count ? in(i) : T(0);
     acc += vals[j];
   }
+  // the warp's total, then the warps' exclusive prefixes across the block
+  const T wtot = warp_sum(acc);
   T tot;
-  T pre = block_exclusive_scan<T>(acc, sm, tot) + sums[blockIdx.x];
+  T pre = block_exclusive_scan<T>(lane == 0 ? wtot : T(0), sm, tot);
+  pre = __shfl_sync(0xffffffffu, pre, 0) + sums[blockIdx.x];
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    if (base + j < count) out(base + j, pre);
-    pre += vals[j];
+    const T inc = warp_inclusive_scan(vals[j]);
+    const uint64_t i = sub + j * 32 + lane;
+    if (i < count) out(i, pre + inc - vals[j]);
+    pre += __shfl_sync(0xffffffffu, inc, 31);
   }
 }
 
