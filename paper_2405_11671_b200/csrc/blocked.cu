@@ -34,6 +34,7 @@
 
 #include "edges.cuh"
 #include "keys.cuh"
+#include "rng.cuh"
 
 namespace gbg {
 
@@ -182,51 +183,86 @@ __global__ void contains_k(G g, const uint32_t* pairs, uint64_t count, uint8_t* 
 // source's current neighbours (the merge slot offset of an inserted arc)
 //
 // With check_sym (the container is symmetric before the batch) it also
-// checks that the batch is closed under reversal: every unique (s, d) with
-// s < d finds (d, s) among the unique keys, and the s < d and s > d counts
-// agree.  A symmetric batch applied to a symmetric container leaves it
+// checks that the batch is closed under reversal: the unique (s, d) with
+// s < d and the reversed unique (d, s) with s > d are the same set (equal
+// counts and equal keyed hash sums).  A symmetric batch applied to a symmetric container leaves it
 // symmetric (an arc is absent/present iff its reverse is), so BFS keeps
 // the cached zero-degree pre-mark after R-MAT batches (bfs_premark).
-__device__ __forceinline__ bool has_key(const uint64_t* k, uint64_t U, uint64_t x) {
-  uint64_t lo = 0, hi = U;
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (k[mid] < x) lo = mid + 1; else hi = mid;
+// first index >= from whose element is >= x (the elements before `from`
+// are < x): exponential steps from `from`, then a binary search
+__device__ __forceinline__ uint32_t gallop_lb(const uint32_t* lst, uint32_t len, uint32_t x, uint32_t from) {
+  uint32_t lo = from, hi = from, step = 1;
+  while (hi < len && lst[hi] < x) {
+    lo = hi + 1;
+    hi = lo + step;
+    step <<= 1;
   }
-  return lo < U && k[lo] == x;
+  if (hi > len) hi = len;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (lst[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
 }
+
+// Each thread takes kFlagArcs consecutive unique arcs: the first one's slot
+// by binary search in its source's list, the next ones (same source,
+// larger targets) by galloping on from the previous slot.  The symmetry
+// check compares two keyed 64-bit hash sums: over the s < d arcs of H(s, d)
+// and over the s > d arcs of H(d, s) (equal sets of unique keys give equal
+// sums; unequal ones collide with probability ~2^-128), plus the counts.
+__device__ __forceinline__ uint64_t sym_hash(uint64_t key, uint64_t salt) { return mix64(key * 0x9e3779b97f4a7c15ull + salt); }
+// kFlagArcs = 1 for small batches, where the chain of searches of one
+// thread would be the critical path
+template <int kFlagArcs>
 __global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t* U_dev, BatchKeys bk,
                               const uint64_t* start, const uint32_t* deg, const uint32_t* pool, int insert,
-                              uint32_t* flag, uint32_t* lb, int check_sym, int* asym, uint64_t* lt,
+                              uint32_t* flag, uint32_t* lb, int check_sym, unsigned long long* hsum, uint64_t* lt,
                               uint64_t* gt) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kFlagArcs;
   const uint64_t U = *U_dev;
   uint32_t nlt = 0, ngt = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
-    if (i >= U) break;
-    const uint64_t x = k[i];
-    const uint32_t s = bk.src(x), d = bk.dst(x);
-    const uint32_t* lst = pool + start[s];
-    const uint32_t len = deg[s];
-    const uint32_t pos = lower_bound_u32(lst, len, d);
-    const bool present = pos < len && lst[pos] == d;
-    flag[i] = insert ? !present : present;
-    lb[i] = pos;
-    if (check_sym) {
-      if (s < d) {
-        ++nlt;
-        if (!has_key(k, U, bk.make(d, s))) *asym = 1;
-      } else {
-        ++ngt;
+  unsigned long long h1 = 0, h2 = 0;
+  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kFlagArcs; i0 < U; i0 += stride) {
+    uint32_t ps = ~0u, ppos = 0;
+#pragma unroll
+    for (int j = 0; j < kFlagArcs; ++j) {
+      const uint64_t i = i0 + j;
+      if (i >= U) break;
+      const uint64_t x = k[i];
+      const uint32_t s = bk.src(x), d = bk.dst(x);
+      const uint32_t* lst = pool + start[s];
+      const uint32_t len = deg[s];
+      const uint32_t pos = s == ps ? gallop_lb(lst, len, d, ppos) : lower_bound_u32(lst, len, d);
+      ps = s;
+      ppos = pos;
+      const bool present = pos < len && lst[pos] == d;
+      flag[i] = insert ? !present : present;
+      lb[i] = pos;
+      if (check_sym) {
+        if (s < d) {
+          ++nlt;
+          h1 += sym_hash(x, 0x243f6a8885a308d3ull);
+          h2 += sym_hash(x, 0x13198a2e03707344ull);
+        } else {
+          ++ngt;
+          const uint64_t y = bk.make(d, s);
+          h1 -= sym_hash(y, 0x243f6a8885a308d3ull);
+          h2 -= sym_hash(y, 0x13198a2e03707344ull);
+        }
       }
     }
   }
   if (check_sym) {
     nlt = __reduce_add_sync(0xffffffffu, nlt);
     ngt = __reduce_add_sync(0xffffffffu, ngt);
+    h1 = warp_sum(h1);
+    h2 = warp_sum(h2);
     if ((threadIdx.x & 31) == 0) {
       if (nlt) atomicAdd(reinterpret_cast<unsigned long long*>(lt), nlt);
       if (ngt) atomicAdd(reinterpret_cast<unsigned long long*>(gt), ngt);
+      if (h1) atomicAdd(hsum, h1);
+      if (h2) atomicAdd(hsum + 1, h2);
     }
   }
 }
@@ -260,11 +296,15 @@ struct HeadOut {
   const uint32_t* A;
   uint32_t* gstart;  // first applied arc of group
   uint32_t* gsrc;
+  uint32_t* agrp;    // group of each applied arc
   __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
-    if (HeadIn{k, bk, A}(i)) {
+    if (i >= *A) return;
+    const bool head = HeadIn{k, bk, A}(i);
+    if (head) {
       gstart[pre] = static_cast<uint32_t>(i);
       gsrc[pre] = bk.src(k[i]);
     }
+    agrp[i] = head ? pre : pre - 1u;
   }
 };
 
@@ -295,52 +335,100 @@ __global__ void group_plan_k(uint64_t count, const uint32_t* ng_dev, const uint3
   }
 }
 
-// old list sizes of touched vertices (for staging)
+// old list sizes of touched vertices; staged_only: only the lists merged in
+// place (a list that grows is merged into a fresh allocation straight from
+// its old one, which stays untouched until the merge is done)
+// A list merged in place keeps its elements before the first applied arc
+// where they are: only [alb[first], deg) is staged.
 struct OldDegIn {
   const uint32_t* gsrc;
   const uint32_t* deg;
   const uint32_t* ng;
-  __device__ __forceinline__ uint64_t operator()(uint64_t gi) const { return gi < *ng ? deg[gsrc[gi]] : 0; }
+  const uint64_t* galloc;
+  const uint32_t* gstart;
+  const uint32_t* alb;
+  int staged_only;
+  __device__ __forceinline__ uint64_t operator()(uint64_t gi) const {
+    if (gi >= *ng) return 0;
+    const uint32_t d = deg[gsrc[gi]];
+    if (!staged_only) return galloc[gi] ? d : 0;  // old elements of lists that grow
+    return galloc[gi] ? 0 : d - alb[gstart[gi]];
+  }
 };
 
 // Staging, merge and set difference run on the balanced segmented
 // expansion (edges.cuh: expand) over the touched groups.
-struct StageOp {  // segments = touched lists, sized by their old degree
+struct StageOp {  // segments = lists merged in place, from their first applied arc's position on
   const uint32_t* gsrc;
   const uint64_t* start;
   const uint32_t* pool;
+  const uint32_t* gstart;
+  const uint32_t* alb;
   uint32_t* staged;
   __device__ __forceinline__ void operator()(uint32_t gi, uint32_t j, uint64_t e) const {
-    staged[e] = pool[start[gsrc[gi]] + j];
+    staged[e] = pool[start[gsrc[gi]] + alb[gstart[gi]] + j];
   }
 };
 
-// old element j of group gi -> its slot in the new list: j plus (insert)
-// or minus (delete) its rank among the group's applied arcs
-struct MergeOldOp {
-  const uint32_t* gsrc;
-  const uint32_t* gstart;
-  const uint64_t* akeys;
-  BatchKeys bk;
+// The old elements of a touched list, cut at the applied arcs' positions in
+// it: segment q covers old elements [begin, begin + len) of group grp, and
+// all of them move by the same shift -- +r (insert: the r applied arcs of
+// the group that sort before them) or -r (delete: the r deleted elements
+// before them, which no segment covers).  Arc i of group gi owns segment
+// i + gi (the old elements just before it), and group gi's tail segment is
+// gstart[gi + 1] + gi.  One balanced expansion over the segments then moves
+// every old element with no search (traversal of neighbor_sets.hpp:339-366's
+// merge / set difference, done element-parallel).
+__global__ void merge_segments_k(uint32_t A, uint32_t ng, const uint32_t* agrp, const uint32_t* gstart,
+                                 const uint32_t* gsrc, const uint32_t* alb, const uint32_t* deg,
+                                 const uint64_t* galloc, int insert, uint64_t* seg_len, uint32_t* seg_begin,
+                                 int32_t* seg_shift, uint32_t* seg_grp, uint32_t* skip) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < A + ng; t += stride) {
+    uint32_t q, gi, begin, end, r;
+    if (t < A) {  // the segment before applied arc t
+      gi = agrp[t];
+      r = t - gstart[gi];
+      q = t + gi;
+      begin = r == 0 ? 0u : alb[t - 1] + (insert ? 0u : 1u);
+      end = alb[t];
+    } else {  // group tail
+      gi = t - A;
+      const uint32_t last = gstart[gi + 1] - 1;
+      r = gstart[gi + 1] - gstart[gi];
+      q = gstart[gi + 1] + gi;
+      begin = alb[last] + (insert ? 0u : 1u);
+      end = deg[gsrc[gi]];
+    }
+    // a list merged in place: its elements before the first applied arc stay
+    if (t < A && r == 0 && !galloc[gi]) {
+      skip[gi] = end;
+      begin = end;
+    }
+    seg_len[q] = end - begin;
+    seg_begin[q] = begin;
+    seg_shift[q] = insert ? static_cast<int32_t>(r) : -static_cast<int32_t>(r);
+    seg_grp[q] = gi;
+  }
+}
+struct MergeSegOp {
+  const uint32_t* seg_grp;
+  const uint32_t* seg_begin;
+  const int32_t* seg_shift;
+  const uint64_t* sscan;  // group -> first staged element (lists merged in place)
   const uint32_t* staged;
+  const uint64_t* galloc;  // != 0: the list grows into a fresh allocation
+  const uint32_t* skip;    // in place: old elements before this stay put (not staged)
+  const uint64_t* start;   // old list starts
+  const uint32_t* gsrc;
   const uint64_t* newstart;
   uint32_t* pool;
-  int insert;
-  __device__ __forceinline__ void operator()(uint32_t gi, uint32_t j, uint64_t e) const {
-    const uint32_t x = staged[e];
-    const uint64_t* b = akeys + gstart[gi];
-    const uint32_t cnt = gstart[gi + 1] - gstart[gi];
-    uint32_t lo = 0, hi = cnt;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (bk.dst(b[mid]) < x) lo = mid + 1; else hi = mid;
-    }
-    uint32_t* out = pool + newstart[gsrc[gi]];
-    if (insert) {
-      out[j + lo] = x;
-    } else if (!(lo < cnt && bk.dst(b[lo]) == x)) {
-      out[j - lo] = x;
-    }
+  __device__ __forceinline__ void operator()(uint32_t q, uint32_t j, uint64_t) const {
+    const uint32_t gi = seg_grp[q];
+    const uint32_t s = gsrc[gi];
+    const uint32_t oi = seg_begin[q] + j;
+    const uint32_t x = galloc[gi] ? pool[start[s] + oi] : staged[sscan[gi] + oi - skip[gi]];
+    pool[newstart[s] + static_cast<int64_t>(oi) + seg_shift[q]] = x;
   }
 };
 
@@ -404,12 +492,13 @@ struct BoundedOut {  // writes [0, n]: the exclusive prefix at n is the total (s
 struct UpdScalars {
   uint64_t U;     // unique, self-loop-free arcs (prepare)
   uint64_t need;  // pool ids the grown lists allocate
-  uint64_t otot;  // old list sizes of the touched sources (staging)
+  uint64_t otot;  // old elements of the touched lists that grow (merged from the pool)
+  uint64_t stot;  // old elements staged: lists merged in place, from their first applied arc on
   uint32_t A;     // applied arcs
   uint32_t ng;    // touched sources
   int bad;        // an endpoint >= n
   int under;      // metadata underflow
-  int asym;       // a unique arc (s, d), s < d, whose reverse is not in the batch
+  unsigned long long hsum[2];  // symmetry hash sums: zero when every unique (s, d) has its reverse
   uint64_t lt, gt;  // unique arcs with s < d / s > d
 };
 
@@ -455,14 +544,21 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint32_t* flag = g->ws.get<uint32_t>("upd.flag", count);
   uint32_t* lb = g->ws.get<uint32_t>("upd.lb", count);
   uint32_t* alb = g->ws.get<uint32_t>("upd.alb", count);
-  GBG_LAUNCH(g, apply_flags_k, grid_for(count, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk, g->bstart,
-             g->bdeg, g->pool, insert ? 1 : 0, flag, lb, g->symmetric ? 1 : 0, &sc->asym, &sc->lt, &sc->gt);
+  if (count >= (1u << 21))
+    GBG_LAUNCH(g, apply_flags_k<4>, grid_for(count / 4 + 1, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk,
+               g->bstart, g->bdeg, g->pool, insert ? 1 : 0, flag, lb, g->symmetric ? 1 : 0, sc->hsum, &sc->lt,
+               &sc->gt);
+  else
+    GBG_LAUNCH(g, apply_flags_k<1>, grid_for(count, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk,
+               g->bstart, g->bdeg, g->pool, insert ? 1 : 0, flag, lb, g->symmetric ? 1 : 0, sc->hsum, &sc->lt,
+               &sc->gt);
   device_scan<uint32_t>(g, BoundedIn<uint32_t, uint64_t>{flag, &sc->U}, ApplyOut{flag, &sc->U, ukeys, lb, akeys, alb},
                         count, &sc->A, "upd.apply");
   // groups by source
   uint32_t* gstart = g->ws.get<uint32_t>("upd.gstart", count + 1);
   uint32_t* gsrc = g->ws.get<uint32_t>("upd.gsrc", count);
-  device_scan<uint32_t>(g, HeadIn{akeys, bk, &sc->A}, HeadOut{akeys, bk, &sc->A, gstart, gsrc}, count, &sc->ng,
+  uint32_t* agrp = g->ws.get<uint32_t>("upd.agrp", count);
+  device_scan<uint32_t>(g, HeadIn{akeys, bk, &sc->A}, HeadOut{akeys, bk, &sc->A, gstart, gsrc, agrp}, count, &sc->ng,
                         "upd.heads");
   tr.mark("presence+groups");
   uint32_t* gcnt = g->ws.get<uint32_t>("upd.gcnt", count);
@@ -471,9 +567,11 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint64_t* galloc = g->ws.get<uint64_t>("upd.galloc", count);
   uint64_t* gascan = g->ws.get<uint64_t>("upd.gascan", count + 1);
   plan_allocations(g, count, gstart, gsrc, insert, sc, gcnt, gnewdeg, gnewcap, galloc, gascan);
-  uint64_t* oscan = g->ws.get<uint64_t>("upd.oscan", count + 1);
-  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng}, BoundedOut<uint64_t, uint32_t>{oscan, &sc->ng},
-                        count + 1, &sc->otot, "upd.oscan");
+  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 0}, NullOut{}, count + 1,
+                        &sc->otot, "upd.oscan");
+  uint64_t* sscan = g->ws.get<uint64_t>("upd.sscan", count + 1);
+  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 1},
+                        BoundedOut<uint64_t, uint32_t>{sscan, &sc->ng}, count + 1, &sc->stot, "upd.sscan");
   UpdScalars h;
   read_scalars(g, sc, sizeof(h), &h);
   tr.mark("plan");
@@ -487,18 +585,36 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
     GBG_LAUNCH(g, refresh_caps_k, grid_for(g->n, 256), 256, 0, g->n, g->bdeg, g->bcap);
     blocked_relayout(g, g->bstart, g->pool, 2 * h.need, true);
     plan_allocations(g, count, gstart, gsrc, insert, sc, gcnt, gnewdeg, gnewcap, galloc, gascan);
-    read_scalars(g, &sc->need, sizeof(h.need), &h.need);
+    device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 1},
+                          BoundedOut<uint64_t, uint32_t>{sscan, &sc->ng}, count + 1, &sc->stot, "upd.sscan");
+    read_scalars(g, sc, sizeof(h), &h);
     if (g->pool_top + h.need > g->pool_cap) fail(GBG_ERR_OOM, "blocked pool exhausted after compaction");
   }
-  // stage the touched old lists
-  const uint64_t otot = h.otot;
-  uint32_t* staged = g->ws.get<uint32_t>("upd.staged", otot);
-  expand(g, oscan, ng, otot, StageOp{gsrc, g->bstart, g->pool, staged});
+  // stage the touched old lists that are merged in place
+  uint32_t* staged = g->ws.get<uint32_t>("upd.staged", h.stot ? h.stot : 1);
+  expand(g, sscan, ng, h.stot, StageOp{gsrc, g->bstart, g->pool, gstart, alb, staged});
   tr.mark("stage");
   // destinations
   uint64_t* newstart = g->ws.get<uint64_t>("upd.newstart", g->n);
   GBG_LAUNCH(g, plan_dest_k, grid_for(ng, 256), 256, 0, ng, gsrc, gascan, galloc, g->pool_top, g->bstart, newstart);
-  expand(g, oscan, ng, otot, MergeOldOp{gsrc, gstart, akeys, bk, staged, newstart, g->pool, insert ? 1 : 0});
+  {
+    const uint32_t nseg = A + ng;
+    uint64_t* seg_len = g->ws.get<uint64_t>("upd.seglen", nseg);
+    uint64_t* seg_scan = g->ws.get<uint64_t>("upd.segscan", nseg + 1);
+    uint32_t* seg_begin = g->ws.get<uint32_t>("upd.segbegin", nseg);
+    int32_t* seg_shift = g->ws.get<int32_t>("upd.segshift", nseg);
+    uint32_t* seg_grp = g->ws.get<uint32_t>("upd.seggrp", nseg);
+    uint32_t* skip = g->ws.get<uint32_t>("upd.skip", ng);
+    GBG_LAUNCH(g, merge_segments_k, grid_for(nseg, 256), 256, 0, A, ng, agrp, gstart, gsrc, alb, g->bdeg, galloc,
+               insert ? 1 : 0, seg_len, seg_begin, seg_shift, seg_grp, skip);
+    device_scan<uint64_t>(g, ArrayIn<uint64_t>{seg_len}, ArrayOut<uint64_t>{seg_scan}, nseg, seg_scan + nseg,
+                          "upd.segs");
+    // old elements that move: all of them (insert), all but the A deleted,
+    // less those that stay in place ahead of a list's first applied arc
+    const uint64_t moved = h.otot + h.stot - (insert ? 0 : A);
+    expand(g, seg_scan, nseg, moved,
+           MergeSegOp{seg_grp, seg_begin, seg_shift, sscan, staged, galloc, skip, g->bstart, gsrc, newstart, g->pool});
+  }
   if (insert) expand(g, gstart, ng, A, MergeNewOp{gsrc, akeys, alb, bk, newstart, g->pool});
   GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,
              g->bcap);
@@ -512,7 +628,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   g->invalidate_derived();
   // a symmetric batch keeps a symmetric container symmetric; anything else
   // is re-verified lazily (graph_is_symmetric)
-  const bool keeps = g->symmetric && !h.asym && h.lt == h.gt;
+  const bool keeps = g->symmetric && h.hsum[0] == 0 && h.hsum[1] == 0 && h.lt == h.gt;
   g->symmetric = keeps;
   g->sym_checked = keeps;
   return A;

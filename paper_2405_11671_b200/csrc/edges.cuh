@@ -93,8 +93,16 @@ __global__ void __launch_bounds__(kEdgeThreads) expand_k(const T* __restrict__ s
       for (int j = 0; j < kEdgeIPT; ++j) {
         if (k0 + j >= len) break;
         if (next <= e0 + k0 + j) {
-          s = seg_of(scan, nseg, e0 + k0 + j, s + 1);
+          // short segments: step a few segments before searching the rest
+          const uint64_t e = e0 + k0 + j;
+          ++s;
           next = scan[s + 1];
+#pragma unroll 1
+          for (int p = 0; p < 3 && next <= e; ++p) next = scan[++s + 1];
+          if (next <= e) {
+            s = seg_of(scan, nseg, e, s + 1);
+            next = scan[s + 1];
+          }
         }
         s_seg[k0 + j] = s;
       }
