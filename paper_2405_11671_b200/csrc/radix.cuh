@@ -65,7 +65,8 @@ static __global__ void __launch_bounds__(kSortThreads) radix_bases_k(uint32_t* h
   }
 }
 
-static __global__ void __launch_bounds__(kSortThreads) radix_onesweep_k(const uint64_t* __restrict__ in,
+template <bool kReload>
+static __global__ void __launch_bounds__(kSortThreads, kReload ? 4 : 3) radix_onesweep_k(const uint64_t* __restrict__ in,
                                                                         uint64_t* __restrict__ out, uint64_t n,
                                                                         int shift, const uint32_t* __restrict__ base,
                                                                         uint64_t* state, unsigned int* tile_ctr) {
@@ -84,15 +85,29 @@ static __global__ void __launch_bounds__(kSortThreads) radix_onesweep_k(const ui
   const uint32_t tile = s_tile;
   const uint64_t base0 = static_cast<uint64_t>(tile) * kSortTile + static_cast<uint64_t>(warp) * kSub;
   const uint32_t lt = (1u << lane) - 1;
-  // 1. each warp: its keys (coalesced, kept in registers) and digit counts
-  uint64_t k[kSortRounds];
+  // 1. each warp: its keys (coalesced) and digit counts.  kReload (large
+  // sorts): the peer masks (lanes of the round with the same digit) are
+  // kept for the ranking and the digits as bytes, and the keys are read
+  // again (L2) for the scatter instead of held in 32 registers -- one
+  // match_any per key instead of two, at 64 registers (4 CTAs per SM).
+  // Otherwise (small sorts, latency-bound) the keys stay in registers.
+  uint32_t pm[kSortRounds];
+  uint32_t dg[kSortRounds / 4];  // four 8-bit digits per word
+  uint64_t k[kReload ? 1 : kSortRounds];
+#pragma unroll
+  for (int r = 0; r < kSortRounds / 4; ++r) dg[r] = 0;
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
     const uint64_t i = base0 + r * 32 + lane;
     const bool valid = i < n;
-    k[r] = valid ? in[i] : ~0ull;
-    const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
+    const uint64_t key = valid ? in[i] : ~0ull;
+    if (!kReload) k[r] = key;
+    const uint32_t d = valid ? static_cast<uint32_t>((key >> shift) & (kRadix - 1)) : kRadix + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (kReload) {
+      pm[r] = peers;
+      dg[r / 4] |= (d & 0xffu) << (8 * (r % 4));
+    }
     if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
     __syncwarp();
   }
@@ -136,10 +151,17 @@ static __global__ void __launch_bounds__(kSortThreads) radix_onesweep_k(const ui
   // 4. each warp ranks its keys in order (stable) into the staged tile
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
-    const bool valid = base0 + r * 32 + lane < n;
-    const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    if (valid) s_keys[s_cnt[warp][d] + __popc(peers & lt)] = k[r];
+    const uint64_t i = base0 + r * 32 + lane;
+    const bool valid = i < n;
+    uint32_t d, peers;
+    if (kReload) {
+      d = (dg[r / 4] >> (8 * (r % 4))) & 0xffu;
+      peers = pm[r];
+    } else {
+      d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
+      peers = __match_any_sync(0xffffffffu, d);
+    }
+    if (valid) s_keys[s_cnt[warp][d] + __popc(peers & lt)] = kReload ? in[i] : k[r];
     __syncwarp();
     if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
     __syncwarp();
@@ -178,8 +200,12 @@ inline uint64_t* radix_sort_u64(gbg_graph* g, uint64_t* keys, uint64_t* scratch,
   uint64_t* dst = scratch;
   for (int p = 0; p < passes; ++p) {
     GBG_CUDA(cudaMemsetAsync(state, 0, static_cast<uint64_t>(ntiles) * kRadix * sizeof(uint64_t), g->stream));
-    GBG_LAUNCH(g, radix_onesweep_k, ntiles, kSortThreads, 0, src, dst, n, p * kRadixBits, hist + p * kRadix, state,
-               ctr + p);
+    if (n > (1u << 20))
+      GBG_LAUNCH(g, radix_onesweep_k<true>, ntiles, kSortThreads, 0, src, dst, n, p * kRadixBits, hist + p * kRadix,
+                 state, ctr + p);
+    else
+      GBG_LAUNCH(g, radix_onesweep_k<false>, ntiles, kSortThreads, 0, src, dst, n, p * kRadixBits, hist + p * kRadix,
+                 state, ctr + p);
     std::swap(src, dst);
   }
   return src;
