@@ -381,8 +381,10 @@ struct StageOp {  // segments = lists merged in place, from their first applied 
 // merge / set difference, done element-parallel).
 __global__ void merge_segments_k(uint32_t A, uint32_t ng, const uint32_t* agrp, const uint32_t* gstart,
                                  const uint32_t* gsrc, const uint32_t* alb, const uint32_t* deg,
-                                 const uint64_t* galloc, int insert, uint64_t* seg_len, uint32_t* seg_begin,
-                                 int32_t* seg_shift, uint32_t* seg_grp, uint32_t* skip) {
+                                 const uint64_t* galloc, const uint64_t* start, const uint64_t* newstart,
+                                 const uint64_t* sscan, const uint32_t* staged, uint32_t* pool, int insert,
+                                 uint64_t* seg_len, uint32_t* seg_begin, const uint32_t** seg_src,
+                                 uint32_t** seg_dst) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < A + ng; t += stride) {
     uint32_t q, gi, begin, end, r;
@@ -400,35 +402,25 @@ __global__ void merge_segments_k(uint32_t A, uint32_t ng, const uint32_t* agrp, 
       begin = alb[last] + (insert ? 0u : 1u);
       end = deg[gsrc[gi]];
     }
-    // a list merged in place: its elements before the first applied arc stay
-    if (t < A && r == 0 && !galloc[gi]) {
-      skip[gi] = end;
-      begin = end;
-    }
+    const uint32_t s = gsrc[gi];
+    const bool grows = galloc[gi] != 0;
+    // a list merged in place: its elements before the first applied arc
+    // stay (and are not staged)
+    if (t < A && r == 0 && !grows) begin = end;
     seg_len[q] = end - begin;
     seg_begin[q] = begin;
-    seg_shift[q] = insert ? static_cast<int32_t>(r) : -static_cast<int32_t>(r);
-    seg_grp[q] = gi;
+    // old element oi of the segment: src[oi] -> dst[oi]
+    seg_src[q] = grows ? pool + start[s] : staged + sscan[gi] - alb[gstart[gi]];
+    seg_dst[q] = pool + newstart[s] + (insert ? static_cast<int64_t>(r) : -static_cast<int64_t>(r));
   }
 }
 struct MergeSegOp {
-  const uint32_t* seg_grp;
   const uint32_t* seg_begin;
-  const int32_t* seg_shift;
-  const uint64_t* sscan;  // group -> first staged element (lists merged in place)
-  const uint32_t* staged;
-  const uint64_t* galloc;  // != 0: the list grows into a fresh allocation
-  const uint32_t* skip;    // in place: old elements before this stay put (not staged)
-  const uint64_t* start;   // old list starts
-  const uint32_t* gsrc;
-  const uint64_t* newstart;
-  uint32_t* pool;
+  const uint32_t* const* seg_src;
+  uint32_t* const* seg_dst;
   __device__ __forceinline__ void operator()(uint32_t q, uint32_t j, uint64_t) const {
-    const uint32_t gi = seg_grp[q];
-    const uint32_t s = gsrc[gi];
     const uint32_t oi = seg_begin[q] + j;
-    const uint32_t x = galloc[gi] ? pool[start[s] + oi] : staged[sscan[gi] + oi - skip[gi]];
-    pool[newstart[s] + static_cast<int64_t>(oi) + seg_shift[q]] = x;
+    seg_dst[q][oi] = seg_src[q][oi];
   }
 };
 
@@ -602,18 +594,16 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
     uint64_t* seg_len = g->ws.get<uint64_t>("upd.seglen", nseg);
     uint64_t* seg_scan = g->ws.get<uint64_t>("upd.segscan", nseg + 1);
     uint32_t* seg_begin = g->ws.get<uint32_t>("upd.segbegin", nseg);
-    int32_t* seg_shift = g->ws.get<int32_t>("upd.segshift", nseg);
-    uint32_t* seg_grp = g->ws.get<uint32_t>("upd.seggrp", nseg);
-    uint32_t* skip = g->ws.get<uint32_t>("upd.skip", ng);
+    const uint32_t** seg_src = g->ws.get<const uint32_t*>("upd.segsrc", nseg);
+    uint32_t** seg_dst = g->ws.get<uint32_t*>("upd.segdst", nseg);
     GBG_LAUNCH(g, merge_segments_k, grid_for(nseg, 256), 256, 0, A, ng, agrp, gstart, gsrc, alb, g->bdeg, galloc,
-               insert ? 1 : 0, seg_len, seg_begin, seg_shift, seg_grp, skip);
+               g->bstart, newstart, sscan, staged, g->pool, insert ? 1 : 0, seg_len, seg_begin, seg_src, seg_dst);
     device_scan<uint64_t>(g, ArrayIn<uint64_t>{seg_len}, ArrayOut<uint64_t>{seg_scan}, nseg, seg_scan + nseg,
                           "upd.segs");
     // old elements that move: all of them (insert), all but the A deleted,
     // less those that stay in place ahead of a list's first applied arc
     const uint64_t moved = h.otot + h.stot - (insert ? 0 : A);
-    expand(g, seg_scan, nseg, moved,
-           MergeSegOp{seg_grp, seg_begin, seg_shift, sscan, staged, galloc, skip, g->bstart, gsrc, newstart, g->pool});
+    expand(g, seg_scan, nseg, moved, MergeSegOp{seg_begin, seg_src, seg_dst});
   }
   if (insert) expand(g, gstart, ng, A, MergeNewOp{gsrc, akeys, alb, bk, newstart, g->pool});
   GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,
