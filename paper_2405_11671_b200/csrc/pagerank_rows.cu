@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(kPrThreads, GBG_PR_MINB) pr_iter_k(PrArgs a) {
   const double base = (1.0 - a.damping) / a.nd + a.damping * dcur / a.nd;
   double err = 0.0;
   // Zero-degree rows (the last class; 7.9M of 16.8M at scale 24) are not
-  // visited: none is anyone's neighbour, and each one's next rank is exactly
+  // visited: they gather nothing (an arc into one on a directed graph reads
+  // the non-positive contrib form pr_init_k leaves in both buffers, i.e.
+  // contributes 0, as the reference's contrib[u] = 0), and each one's next rank is exactly
   // `base` (base + damping * 0), so their dangling mass is n_zero * base and
   // their L1 step is n_zero * |base - previous base|, folded in below, and
   // the output maps them to the last base (pr_to_p_k).
