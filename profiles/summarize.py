@@ -71,7 +71,14 @@ def full(rep, out_md, json_path=None):
         for k, s in sorted(stalls, key=lambda x: -x[1])[:6]:
             lines.append(f"- {100 * s / tot:.1f}% {k.replace('smsp__pcsamp_warps_issue_stalled_', '')}")
         lines.append("")
-        short = name.split("(")[0].split("::")[-1].split("<")[0]
+        base = name.split("(")[0]
+        depth, plain = 0, ""
+        for ch in base:  # drop template arguments, then namespaces and "void "
+            depth += ch == "<"
+            if depth == 0:
+                plain += ch
+            depth -= ch == ">"
+        short = plain.split("::")[-1].split()[-1]
         if "dram__bytes_read.sum" in d:
             summary[short] = {"dram_bytes_per_launch": to_bytes(d["dram__bytes_read.sum"]) +
                               to_bytes(d.get("dram__bytes_write.sum", ("0", "byte"))),

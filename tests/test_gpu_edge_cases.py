@@ -318,6 +318,19 @@ def test_symmetric_batches_keep_the_premark(gbg, ref, orc):
     rg = ref.csr(nn, off, nbr)
     for src in range(0, n, 7):
         assert np.array_equal(gbg.bfs(g, src).depth, rg.bfs(src))
+    # equal s < d / s > d counts but not reverse-closed: (2, n) and (n+1, 3)
+    # reach the two isolated vertices n, n+1 one way each; the symmetry
+    # check must see it (hash sums), or the zero-out-degree pre-mark would
+    # hide vertex n from a BFS from 2
+    nn2, pairs2 = undirected(n, [(i, (i * 7 + 3) % n) for i in range(n)], orc)
+    g2 = gbg.BlockedGraph.build(n + 2, pairs2)
+    assert gbg.bfs(g2, 2).depth[n] == -1
+    g2.insert_batch(np.array([[2, n], [n + 1, 3]], dtype=np.uint32))
+    off, nbr = g2.to_csr()
+    rg2 = ref.csr(n + 2, off, nbr)
+    for src in (2, 3, n + 1, n):
+        assert np.array_equal(gbg.bfs(g2, src).depth, rg2.bfs(src)), src
+    assert gbg.bfs(g2, 2).depth[n] == 1
 
 
 def test_batch_self_loop_with_out_of_range_id_is_dropped(gbg, ref):
