@@ -357,12 +357,16 @@ def run_updates(torch, gbg, S, warmup, sizes, reps=3, cpu=None):
             torch.cuda.synchronize()
             rows_first = time.perf_counter() - t0
             t_rows = events_time(torch, g.stream(), lambda: gbg.pagerank_device(g, out.data_ptr(), 0.85, 20, TINY), 3) / 3
+            rows_bytes = gbg.pagerank_index_bytes(g)[1]
             index_ms = gbg.pagerank_prepare(g)
+            tiled_bytes = gbg.pagerank_index_bytes(g)[0]
             t_tiled = events_time(torch, g.stream(), lambda: gbg.pagerank_device(g, out.data_ptr(), 0.85, 20, TINY), 3) / 3
             g.delete_batch_device(dev.data_ptr(), dev.shape[0])
             res["pagerank_after_insert_1e6"] = {
                 "rows_first_call_ms": rows_first * 1e3, "rows_call_ms": t_rows * 1e3,
                 "tiled_index_build_ms": index_ms, "tiled_call_ms": t_tiled * 1e3,
+                "rows_layout_bytes": rows_bytes, "tiled_index_bytes": tiled_bytes,
+                "container_bytes": g.memory_bytes(),
                 "note": "s22 blocked container after the 10^6 rep-0 insert; 20 iterations"}
     return res, g
 
@@ -546,7 +550,8 @@ def main():
     g = gbg.generate_rmat(S, 16 << S, 1, *RMAT)
     n, m = g.num_vertices(), g.num_edges()
     layout_ms = gbg.pagerank_prepare(g)  # tiled index: container-side, cached, dropped by updates
-    log(f"pagerank index build: {layout_ms:.1f} ms")
+    layout_bytes = gbg.pagerank_index_bytes(g)[0]
+    log(f"pagerank index build: {layout_ms:.1f} ms, {layout_bytes / 1e9:.2f} GB")
     barrier(world)
     with Clocks(local) as clk:
         t_step, launches, pr_out = run_pagerank(torch, gbg, g, args.steps, args.warmup)
@@ -742,6 +747,7 @@ def main():
                 "roofline_bfs": roofline_bfs, "roofline_updates": roofline_upd,
                 "value_incl_layout": world * 20 * m / (t_max + layout_ms / 1e3) / 1e9,
                 "layout_build_ms": layout_ms,
+                "layout_bytes": layout_bytes, "container_bytes": g.memory_bytes(),
                 "layout_note": "value = calls on the prepared tiled index (built once per graph version, "
                                "layout_build_ms); value_incl_layout charges one index build to one call; "
                                "one-shot calls use the row path (pagerank_rows), which e2e measures",

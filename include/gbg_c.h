@@ -202,6 +202,10 @@ gbg_status gbg_pagerank_device(gbg_graph* g, double damping, uint64_t max_iters,
  * renumbered by degree, see pagerank.cu — ahead of the first gbg_pagerank
  * call; *build_ms = its one-time device build time.  Invalidated by updates. */
 gbg_status gbg_pagerank_prepare(gbg_graph* g, double* build_ms);
+/* Device bytes held by the handle's cached PageRank indexes (0 when not
+ * built): the tiled index gbg_pagerank_prepare builds and the relabelled row
+ * layout one-shot calls build.  Both are derived data, dropped on updates. */
+gbg_status gbg_pagerank_index_bytes(const gbg_graph* g, uint64_t* tiled, uint64_t* rows);
 /* gb::cc (algorithms.cpp:194-234): labels = minimum vertex id of each
  * component. */
 gbg_status gbg_cc(gbg_graph* g, uint32_t* labels);

@@ -285,7 +285,9 @@ void pr_layout_free(PrRows* L);
 PrRows* pr_layout(gbg_graph* g);
 uint64_t pagerank_rows_run(gbg_graph* g, double damping, uint64_t max_iters, double tol, double* p_dev);
 double rows_build_ms(const PrRows* L);
+uint64_t rows_bytes(const PrRows* L);
 }  // namespace prrows
+uint64_t pr_layout_bytes(const PrLayout* L);  // pagerank.cu
 
 // Optional phase timing (environment GBG_TRACE=1): CUDA events on the
 // handle's stream at named points, device-time deltas printed to stderr

@@ -1104,6 +1104,13 @@ gbg_status gbg_pagerank_device(gbg_graph* g, double damping, uint64_t max_iters,
                                uint64_t* iterations) {
   return pagerank_entry(g, damping, max_iters, tolerance, ranks_dev, false, iterations);
 }
+gbg_status gbg_pagerank_index_bytes(const gbg_graph* g, uint64_t* tiled, uint64_t* rows) {
+  return guard([&] {
+    if (!g) fail(GBG_ERR_INVALID_ARGUMENT, "null handle");
+    if (tiled) *tiled = pr_layout_bytes(g->pr);
+    if (rows) *rows = prrows::rows_bytes(g->pr_rows);
+  });
+}
 gbg_status gbg_pagerank_prepare(gbg_graph* g, double* build_ms) {
   return guard([&] {
     GBG_HANDLE(g);

@@ -632,6 +632,12 @@ uint64_t pagerank_rows_run(gbg_graph* g, double damping, uint64_t max_iters, dou
   return done;
 }
 
+uint64_t rows_bytes(const PrRows* L) {
+  if (!L) return 0;
+  // relabelled CSR and both id maps (the heavy-row chunk tables are small)
+  return (L->n + 1) * 8 + L->m * 4 + L->n * 8;
+}
+
 double rows_build_ms(const PrRows* L) { return L->build_ms; }
 }  // namespace prrows
 }  // namespace gbg

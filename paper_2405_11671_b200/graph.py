@@ -156,6 +156,7 @@ _SIGS = {
     "gbg_update_batch_device": [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_uint64, _vp],
     "gbg_contains_device": [_vp, _vp, C.c_uint64, _vp],
     "gbg_pagerank_prepare": [_vp, _f64p],
+    "gbg_pagerank_index_bytes": [_vp, _u64p, _u64p],
     "gbg_bc": [_vp, C.c_uint32, _f64p],
     "gbg_bc_device": [_vp, C.c_uint32, _vp],
     "gbg_kcore": [_vp, _u64p],
@@ -494,6 +495,13 @@ def pagerank_prepare(g: _Graph) -> float:
     ms = C.c_double()
     _check(_L.gbg_pagerank_prepare(g.handle, C.byref(ms)))
     return ms.value
+
+
+def pagerank_index_bytes(g: _Graph) -> tuple:
+    """(tiled index bytes, row layout bytes) currently cached on the handle."""
+    a, b = C.c_uint64(), C.c_uint64()
+    _check(_L.gbg_pagerank_index_bytes(g.handle, C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def pagerank_device(g: _Graph, out_ptr: int, damping=0.85, max_iters=20, tolerance=1e-4) -> int:

@@ -342,3 +342,19 @@ def test_batch_self_loop_with_out_of_range_id_is_dropped(gbg, ref):
     assert g.num_edges() == 4
     with pytest.raises(IndexError):
         g.insert_batch(np.array([[2, 9]], dtype=np.uint32))
+
+
+def test_pagerank_index_bytes_and_invalidation(gbg, orc):
+    """The cached PageRank indexes report their device bytes, and an update
+    drops both (derived data of one graph version)."""
+    n, pairs = orc.rmat(12, 16 << 12, 3)
+    g = gbg.BlockedGraph.build(n, pairs)
+    assert gbg.pagerank_index_bytes(g) == (0, 0)
+    gbg.pagerank(g, 0.85, 3, 1e-300)  # one-shot call: row layout
+    tiled, rows = gbg.pagerank_index_bytes(g)
+    assert tiled == 0 and rows >= 4 * g.num_edges()
+    gbg.pagerank_prepare(g)
+    tiled, rows = gbg.pagerank_index_bytes(g)
+    assert tiled >= 2 * g.num_edges()
+    g.insert_batch(np.array([[0, n - 1], [n - 1, 0]], dtype=np.uint32))
+    assert gbg.pagerank_index_bytes(g) == (0, 0)
