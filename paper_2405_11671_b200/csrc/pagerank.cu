@@ -70,7 +70,7 @@ constexpr uint16_t kRunStart = 0x8000;      // arc word: run-start bit | row in 
 constexpr uint32_t kGroup = 256;            // arcs per warp work item (8 rounds of 32)
 constexpr int kConsumers = 31;              // consumer warps; warp 31 issues the bulk copies
 #ifndef GBG_PR_WARP_GROUPS
-#define GBG_PR_WARP_GROUPS 2
+#define GBG_PR_WARP_GROUPS 1
 #endif
 constexpr uint32_t kWarpGroups = GBG_PR_WARP_GROUPS;            // groups per consumer warp per chunk
 constexpr uint32_t kChunkGroups = kConsumers * kWarpGroups;     // groups per staged chunk at most
@@ -87,9 +87,13 @@ constexpr uint32_t kGrpBuf = (kChunkGroups + 8 + 3) & ~3u;  // staged group run 
 constexpr int kStages = GBG_PR_STAGES;
       // shared-memory ring depth
 #ifndef GBG_PR_TILE_ARCS
-#define GBG_PR_TILE_ARCS (1u << 17)
+#define GBG_PR_TILE_ARCS (1u << 19)
 #endif
 constexpr uint32_t kTileArcs = GBG_PR_TILE_ARCS;
+#ifndef GBG_PR_MIN_TILES_PER_SM
+#define GBG_PR_MIN_TILES_PER_SM 4
+#endif
+constexpr uint32_t kMinTilesPerSm = GBG_PR_MIN_TILES_PER_SM;
 #ifndef GBG_PR_THREADS
 #define GBG_PR_THREADS 1024
 #endif
@@ -276,17 +280,18 @@ __global__ void block_starts_k(const uint64_t* k, const uint64_t* run_off, uint6
 }
 
 // tile start: the block's first run, or a run whose arc offset in the block
-// crosses a multiple of kTileArcs
+// crosses a multiple of the tile size (2^tile_bits arcs)
 struct TileIn {
   const uint64_t* k;
   const uint64_t* run_off;
   const uint64_t* block_arc;
   int shift;
+  int tile_bits;
   __device__ __forceinline__ bool start(uint64_t r) const {
     const uint32_t b = run_block(k, run_off, r, shift);
     if (r == 0 || run_block(k, run_off, r - 1, shift) != b) return true;
     const uint64_t base = block_arc[b];
-    return (run_off[r] - base) / kTileArcs != (run_off[r - 1] - base) / kTileArcs;
+    return (run_off[r] - base) >> tile_bits != (run_off[r - 1] - base) >> tile_bits;
   }
   __device__ __forceinline__ uint32_t operator()(uint64_t r) const { return start(r) ? 1u : 0u; }
 };
@@ -437,7 +442,12 @@ void layout_finish(gbg_graph* g, PrLayout* L) {
   // 3. blocks and tiles
   uint64_t* block_arc = g->ws.get<uint64_t>("prl.blockarc", L->nblocks);
   GBG_LAUNCH(g, block_starts_k, grid_for(nruns, 256), 256, 0, k, run_off, nruns, shift, block_arc);
-  TileIn tin{k, run_off, block_arc, shift};
+  // tiles of up to kTileArcs arcs, smaller on small graphs so that there
+  // are at least kMinTilesPerSm tiles per SM to balance over
+  int tile_bits = 0;
+  while ((2ull << tile_bits) <= kTileArcs) ++tile_bits;
+  while (tile_bits > 16 && (m >> tile_bits) < uint64_t{kMinTilesPerSm} * g->sm_count) --tile_bits;
+  TileIn tin{k, run_off, block_arc, shift, tile_bits};
   device_scan<uint32_t>(g, tin, NullOut{}, nruns, cnt + 1, "prl.tiles");
   read_scalars(g, cnt + 1, sizeof(uint32_t), &L->ntiles);
   L->tile_arc = dalloc<uint64_t>(L->ntiles + 1);
@@ -635,6 +645,17 @@ constexpr size_t kSmemStage = kArcBuf * 2 + kRunBuf * 4 + kGrpBuf * 4;
 constexpr size_t kSmemBytes = kSmemAcc + kStages * kSmemStage;
 static_assert(kSmemStage % 16 == 0, "stage alignment");
 
+#ifdef GBG_PR_TRACE
+// timing trace (analysis builds only): per CTA up to 64 tiles of
+// {block, arcs, t_first_chunk, t_groups_done, t_finalized, smid}
+__device__ unsigned long long g_pr_trace[148 * 64 * 6];
+__device__ unsigned g_pr_trace_n[148];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 struct StageInfo {
   PrChunk ch;
   uint64_t abase;  // arc index of the stage's first staged word
@@ -836,6 +857,24 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
       const uint32_t qbase = s_stage[s].qbase;
       const uint32_t row0 = ch.block * kRows;
       const uint32_t nrows = min(kRows, a.nz - row0);
+#ifdef GBG_PR_TRACE
+      if (ctid == 0 && (ch.flags & (1u << 8))) {
+        const unsigned k = g_pr_trace_n[blockIdx.x]++;
+        if (k < 64) {
+          unsigned long long* r = g_pr_trace + (blockIdx.x * 64 + k) * 6;
+          r[0] = ch.block;
+          r[1] = 0;
+          r[2] = gtime();
+          unsigned smid;
+          asm("mov.u32 %0, %smid;" : "=r"(smid));
+          r[5] = smid;
+        }
+      }
+      if (ctid == 0) {
+        const unsigned k = g_pr_trace_n[blockIdx.x] - 1;
+        if (k < 64) g_pr_trace[(blockIdx.x * 64 + k) * 6 + 1] += ch.len;
+      }
+#endif
       if (ch.flags & (1u << 8)) {  // the tile's first chunk: clear the sums
         for (uint32_t i = ctid; i < nrows; i += kCT) s_lo[i] = s_hi[i] = 0u;
         consumer_sync();
@@ -869,6 +908,10 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
       if (lane == 0) mbar_arrive(&s_empty[s]);
       if (ch.flags & (1u << 9)) {  // the tile's last chunk: finalize or flush
         consumer_sync();
+#ifdef GBG_PR_TRACE
+        if (ctid == 0 && g_pr_trace_n[blockIdx.x] - 1 < 64)
+          g_pr_trace[(blockIdx.x * 64 + g_pr_trace_n[blockIdx.x] - 1) * 6 + 3] = gtime();
+#endif
         double err = 0.0;
         bool fin = false;
         const uint32_t b = ch.block;
@@ -904,6 +947,10 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
           if (ctid == 0) a.blk_err[b] = be;
         }
         consumer_sync();
+#ifdef GBG_PR_TRACE
+        if (ctid == 0 && g_pr_trace_n[blockIdx.x] - 1 < 64)
+          g_pr_trace[(blockIdx.x * 64 + g_pr_trace_n[blockIdx.x] - 1) * 6 + 4] = gtime();
+#endif
       }
     }
   }
@@ -1104,6 +1151,20 @@ gbg_status gbg_pagerank_device(gbg_graph* g, double damping, uint64_t max_iters,
                                uint64_t* iterations) {
   return pagerank_entry(g, damping, max_iters, tolerance, ranks_dev, false, iterations);
 }
+#ifdef GBG_PR_TRACE
+// analysis builds only: copy out and reset the per-CTA tile trace of the
+// last pr_tile_k launch ([148][64][6] u64 + [148] counts)
+gbg_status gbg_debug_pr_trace(unsigned long long* out, unsigned* counts) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_pr_trace, sizeof(g_pr_trace));
+  cudaMemcpyFromSymbol(counts, g_pr_trace_n, sizeof(g_pr_trace_n));
+  static unsigned zero[148] = {};
+  cudaMemcpyToSymbol(g_pr_trace_n, zero, sizeof(zero));
+  static unsigned long long z2[148 * 64 * 6] = {};
+  cudaMemcpyToSymbol(g_pr_trace, z2, sizeof(z2));
+  return GBG_OK;
+}
+#endif
 gbg_status gbg_pagerank_index_bytes(const gbg_graph* g, uint64_t* tiled, uint64_t* rows) {
   return guard([&] {
     if (!g) fail(GBG_ERR_INVALID_ARGUMENT, "null handle");
