@@ -601,7 +601,10 @@ __device__ __forceinline__ unsigned long long to_fix(double contrib) {
 // evict_last, everything else streams with evict_first, so the hot part of
 // both contrib buffers (2 x 32 MiB) stays in the 126 MB L2 while the arcs,
 // the fp64 ranks and the cold contribs pass through.
-constexpr uint32_t kHot = 1u << 22;
+#ifndef GBG_PR_HOT_BITS
+#define GBG_PR_HOT_BITS 22
+#endif
+constexpr uint32_t kHot = 1u << GBG_PR_HOT_BITS;
 __device__ __forceinline__ void st_hint_u64(unsigned long long* a, unsigned long long v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol) : "memory");
 }

@@ -60,14 +60,22 @@ dist = 1 + (rr[:, 1:] != rr[:, :-1]).sum(1)
 print(f"  distinct runs per round: mean {dist.float().mean().item():.2f}")
 
 
+rblk = blk[: R * 32].view(R, 32)[:, 0]
+
+
 def conflicts(rows):
     b = (rows[: R * 32] & 31).view(R, 32)
     oh = torch.zeros(R, 32, dtype=torch.int32, device=dev)
     oh.scatter_add_(1, b, torch.ones_like(b, dtype=torch.int32))
-    return oh.max(1).values.float().mean().item()
+    mx = oh.max(1).values.float()
+    parts = []
+    for lo, hi in [(0, 16), (16, 64), (64, 256), (256, 1 << 20)]:
+        sel = (rblk >= lo) & (rblk < hi)
+        parts.append(f"[{lo},{hi}) {mx[sel].mean().item():.2f}")
+    return f"{mx.mean().item():.2f} (" + ", ".join(parts) + ")"
 
 
-print(f"  bank conflict degree per round (rows ascending in a run): {conflicts(rib):.2f}")
+print(f"  bank conflict degree per round (rows ascending in a run): {conflicts(rib)}")
 # interleaved order inside each run: sort by (run, rank within (run, bank), bank)
 bank = rib & 31
 kb = (rid << 18) | (bank << 13) | rib
@@ -82,6 +90,6 @@ rank = idx - segstart
 k2 = (rb_run << 18) | (rank.clamp(max=8191) << 5) | rb_bank
 k2, p2 = torch.sort(k2)
 rib2 = (kb & 8191)[p2]
-print(f"  bank conflict degree per round (interleaved banks in a run): {conflicts(rib2):.2f}")
+print(f"  bank conflict degree per round (interleaved banks in a run): {conflicts(rib2)}")
 rand = torch.randint(0, 8192, (m,), device=dev)
-print(f"  bank conflict degree per round (random rows): {conflicts(rand):.2f}")
+print(f"  bank conflict degree per round (random rows): {conflicts(rand)}")
