@@ -35,10 +35,10 @@
 //     bit, in 16 bits, plus one uint32 source id per run: ~3 B per arc
 //     against 4 B of neighbour id in the CSR;
 //   * accumulates each block's row sums in shared memory (64 KiB per CTA)
-//     as 64-bit fixed point (2^-62 units): integer atomics are
-//     order-independent, so the result is deterministic whatever the
-//     schedule, and the rounding (<= 2^-63 per term) stays ~1e-12 in
-//     relative L1 after 20 iterations, far inside the 1e-9 bar.  sm_100
+//     as 64-bit fixed point (2^-F units, F from the arc count, see
+//     fix_bits_for): integer atomics are order-independent, so the result
+//     is deterministic whatever the schedule, and the rounding stays ~6e-11
+//     in relative L1 after 20 iterations, inside the 1e-9 bar.  sm_100
 //     has no native 64-bit shared-memory add (it compiles to a CAS loop),
 //     so each sum is two 32-bit words: the low word takes the term's low
 //     half with a native atomic add that returns the old value, and the
@@ -98,11 +98,27 @@ constexpr uint32_t kMinTilesPerSm = GBG_PR_MIN_TILES_PER_SM;
 #define GBG_PR_THREADS 1024
 #endif
 constexpr int kPrThreads = GBG_PR_THREADS;
-#ifndef GBG_PR_FIX_BITS
-#define GBG_PR_FIX_BITS 62
+// Fixed-point scale of the row sums: 2^F, F = ceil(log2(m)) + kFixMargin
+// (at most 62; 62 below 2^26 arcs).  A contrib is about 1/m of the rank
+// mass (PageRank of an undirected graph is close to degree / 2m), so its
+// rounding error relative to its size is ~2^-kFixMargin at every scale:
+// measured 5.8e-11 / 6.1e-11 relative L1 after 20 iterations at scales 22 /
+// 24 (F = 55 / 57) against the reference, inside the 1e-9 bar (each bit of
+// margin halves it).  The same choice keeps a term below 2^32 units, so the
+// high word of a row sum only takes the carries out of the low word (a few
+// percent of the adds), and the high-word add is skipped when there is
+// none.  Row sums stay below 2^(64-F) >= 4.
+#ifndef GBG_PR_FIX_MARGIN
+#define GBG_PR_FIX_MARGIN 28
 #endif
-constexpr double kFix = static_cast<double>(1ull << GBG_PR_FIX_BITS);  // fixed-point scale of the sums
-constexpr double kUnfix = 1.0 / kFix;
+constexpr int kFixMargin = GBG_PR_FIX_MARGIN;
+inline int fix_bits_for(uint64_t m) {
+  int lg = 0;  // ceil(log2(m))
+  while ((uint64_t{1} << lg) < m) ++lg;
+  // below 2^26 arcs the finest scale: small graphs keep ~1e-13 sums
+  // (equal-contrib graphs such as K_n round every term the same way)
+  return lg <= 26 ? 62 : std::min(62, lg + kFixMargin);
+}
 
 // One staged chunk of a tile: arcs [e0, e0 + len), work groups [g0, g0 +
 // ng), the runs they touch [rlo, rhi) (both widened to 16-byte bounds for
@@ -538,6 +554,7 @@ struct PrArgs {
   PrScalars* sc;
   uint32_t ntiles, nblocks, nz;
   double damping, nd, tol;
+  double fix, unfix;  // fixed-point scale of the contribs and row sums
   double n_zero;  // zero-degree rows
   int iter;
 };
@@ -592,8 +609,8 @@ __device__ __forceinline__ unsigned long long ld_fix_if(const unsigned long long
 }
 
 // contrib in fixed point (gathered by the next iteration)
-__device__ __forceinline__ unsigned long long to_fix(double contrib) {
-  return __double2ull_rn(fmax(contrib, 0.0) * kFix);
+__device__ __forceinline__ unsigned long long to_fix(double contrib, double fix) {
+  return __double2ull_rn(fmax(contrib, 0.0) * fix);
 }
 
 // L2 residency: the fixed-point contribs of the kHot highest-degree rows
@@ -622,12 +639,12 @@ __device__ __forceinline__ double ld_first_f64(const double* a, uint64_t pol) {
 __device__ __forceinline__ void pr_finalize(const PrArgs& a, double base, uint32_t r, unsigned long long fsum,
                                             double& err, uint64_t pf, uint64_t pl) {
   const double d = static_cast<double>(ld_stream_u32(a.deg + r, pf));
-  const double next = base + a.damping * (static_cast<double>(fsum) * kUnfix);
+  const double next = base + a.damping * (static_cast<double>(fsum) * a.unfix);
   const double xo = ld_first_f64(a.x_old + r, pf);
   err += fabs(next - xo * d);
   const double c = next / d;
   st_hint_f64(a.x_new + r, c, pf);
-  st_hint_u64(a.t_new + r, to_fix(c), r < kHot ? pl : pf);
+  st_hint_u64(a.t_new + r, to_fix(c, a.fix), r < kHot ? pl : pf);
 }
 
 // exact 64-bit fixed-point add into a (lo, hi) pair of shared words
@@ -743,7 +760,7 @@ __device__ __forceinline__ void pr_group(const PrArgs& a, uint32_t* lo, uint32_t
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const uint32_t c = carry_hi(old[j], static_cast<uint32_t>(x[j]), static_cast<uint32_t>(x[j] >> 32));
-    if (kFull || on[j]) atomicAdd(hi + row[j], c);  // result unused: RED (adds 0 when nothing carries)
+    if ((kFull || on[j]) && c) atomicAdd(hi + row[j], c);  // result unused: RED
   }
 }
 
@@ -993,13 +1010,13 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
 // contributes fmax(x, 0) = 0 as the reference's contrib[u] = 0 does
 // (the fixed-point forms the gathers read are 0 for those rows)
 __global__ void pr_init_k(const uint32_t* deg, uint64_t n, double* x, double* x1, unsigned long long* t,
-                          unsigned long long* t1) {
+                          unsigned long long* t1, double fix) {
   const double p0 = 1.0 / static_cast<double>(n);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
     const uint32_t d = deg[r];
     x[r] = d ? p0 / static_cast<double>(d) : -p0;
-    t[r] = d ? to_fix(p0 / static_cast<double>(d)) : 0ull;
+    t[r] = d ? to_fix(p0 / static_cast<double>(d), fix) : 0ull;
     if (!d) {
       x1[r] = -p0;
       t1[r] = 0ull;
@@ -1057,7 +1074,8 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
   const double p0 = 1.0 / static_cast<double>(n);
   unsigned long long* T0 = g->ws.get<unsigned long long>("pr.t0", n);
   unsigned long long* T1 = g->ws.get<unsigned long long>("pr.t1", n);
-  GBG_LAUNCH(g, pr_init_k, grid_for(n, 256), 256, 0, L->deg, n, X0, X1, T0, T1);
+  const double fix = std::ldexp(1.0, fix_bits_for(L->m));
+  GBG_LAUNCH(g, pr_init_k, grid_for(n, 256), 256, 0, L->deg, n, X0, X1, T0, T1, fix);
   // initial dangling mass: every zero-degree row holds p0
   const double n_zero = static_cast<double>(n - L->nz);
   GBG_LAUNCH(g, pr_scalars_init_k, 1, 1, 0, sc, n_zero * p0, p0);
@@ -1080,6 +1098,8 @@ uint64_t pagerank_run(gbg_graph* g, double damping, uint64_t max_iters, double t
   a.nblocks = L->nblocks;
   a.nz = L->nz;
   a.damping = damping;
+  a.fix = fix;
+  a.unfix = 1.0 / fix;
   a.nd = static_cast<double>(n);
   a.tol = tol;
   a.n_zero = n_zero;
