@@ -178,6 +178,77 @@ static __global__ void __launch_bounds__(kSortThreads, kReload ? 4 : 3) radix_on
   }
 }
 
+// ---- small sorts (n <= kSmallMax): two launches instead of a histogram
+// pass and one onesweep launch per digit (a 10^4-edge update batch sorts
+// 2 * 10^4 keys, where the digit passes are pure launch + look-back
+// latency).  Tiles of 4096 keys are bitonic-sorted in shared memory as
+// (masked key << 12 | index in tile) -- the index makes the order stable;
+// then every CTA loads all sorted tiles into shared memory and places each
+// key of its tile by binary searches in the other tiles (keys of earlier
+// tiles first on ties).
+constexpr uint32_t kSmallTile = 4096;
+constexpr uint32_t kSmallMax = 24576;  // all keys in the merge CTA's shared memory (192 KB)
+constexpr int kSmallThreads = 1024;
+
+static __global__ void __launch_bounds__(kSmallThreads) small_sort_tiles_k(const uint64_t* __restrict__ in,
+                                                                          uint64_t n, uint64_t mask,
+                                                                          uint64_t* __restrict__ tmp) {
+  __shared__ uint64_t s[kSmallTile];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kSmallTile;
+  const uint32_t len = static_cast<uint32_t>(n - base < kSmallTile ? n - base : kSmallTile);
+  for (uint32_t i = threadIdx.x; i < kSmallTile; i += kSmallThreads)
+    s[i] = i < len ? ((in[base + i] & mask) << 12) | i : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= kSmallTile; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < kSmallTile; i += kSmallThreads) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = s[i], b = s[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < len; i += kSmallThreads) tmp[base + i] = s[i];
+}
+
+static __global__ void __launch_bounds__(kSmallThreads) small_merge_k(const uint64_t* __restrict__ tmp,
+                                                                     const uint64_t* __restrict__ in, uint64_t n,
+                                                                     uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t s_all[];
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallThreads) s_all[i] = tmp[i];
+  __syncthreads();
+  const uint32_t ntiles = static_cast<uint32_t>((n + kSmallTile - 1) / kSmallTile);
+  const uint32_t c = blockIdx.x;
+  const uint32_t base = c * kSmallTile;
+  const uint32_t len = static_cast<uint32_t>(n - base < kSmallTile ? n - base : kSmallTile);
+  for (uint32_t i = threadIdx.x; i < len; i += kSmallThreads) {
+    const uint64_t v = s_all[base + i];
+    const uint64_t key = v >> 12;
+    uint32_t pos = i;
+    for (uint32_t o = 0; o < ntiles; ++o) {
+      if (o == c) continue;
+      uint32_t lo = o * kSmallTile;
+      uint32_t hi = lo + static_cast<uint32_t>(n - lo < kSmallTile ? n - lo : kSmallTile);
+      const uint32_t t0 = lo;
+      // count of keys < key (later tiles) or <= key (earlier tiles)
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint64_t km = s_all[mid] >> 12;
+        if (o < c ? km <= key : km < key) lo = mid + 1;
+        else hi = mid;
+      }
+      pos += lo - t0;
+    }
+    out[pos] = in[base + (v & (kSmallTile - 1))];
+  }
+}
+
 // Sorts keys[0..n) by their low `bits` bits (stable); scratch must hold n
 // keys.  Returns the buffer holding the result (keys or scratch).
 inline uint64_t* radix_sort_u64(gbg_graph* g, uint64_t* keys, uint64_t* scratch, uint64_t n, int bits,
@@ -186,6 +257,19 @@ inline uint64_t* radix_sort_u64(gbg_graph* g, uint64_t* keys, uint64_t* scratch,
   if (n > 0xffffffffull) fail(GBG_ERR_INVALID_ARGUMENT, "radix sort: more than 2^32-1 keys");
   const int passes = (bits + kRadixBits - 1) / kRadixBits;
   if (passes > kMaxPasses) fail(GBG_ERR_LOGIC, "radix sort: too many digit passes");
+  if (n <= kSmallMax && bits <= 51) {
+    static bool attr = [] {
+      cudaFuncSetAttribute(small_merge_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kSmallMax * sizeof(uint64_t)));
+      return true;
+    }();
+    (void)attr;
+    uint64_t* tmp = g->ws.get<uint64_t>(std::string(tag) + ".small", n);
+    const unsigned nt = static_cast<unsigned>((n + kSmallTile - 1) / kSmallTile);
+    GBG_LAUNCH(g, small_sort_tiles_k, nt, kSmallThreads, 0, keys, n, (uint64_t{1} << bits) - 1, tmp);
+    GBG_LAUNCH(g, small_merge_k, nt, kSmallThreads, n * sizeof(uint64_t), tmp, keys, n, scratch);
+    return scratch;
+  }
   const uint32_t ntiles = static_cast<uint32_t>((n + kSortTile - 1) / kSortTile);
   const std::string t(tag);
   uint32_t* hist = g->ws.get<uint32_t>(t + ".hist", kMaxPasses * kRadix);

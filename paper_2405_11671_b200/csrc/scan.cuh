@@ -132,10 +132,53 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_k(In in, Out out, uint
   }
 }
 
+// Small scans (count <= kSmallScan): one CTA of 1024 threads walks the
+// items in tiles of 16K (same warp-striped rounds as scan_down_k) and
+// carries the running prefix -- one launch instead of three, for the
+// latency-bound scans of small update batches and small graphs.
+constexpr int kSmallScanThreads = 1024;
+constexpr uint64_t kSmallScanTile = static_cast<uint64_t>(kSmallScanThreads) * kScanItems;
+constexpr uint64_t kSmallScan = 2 * kSmallScanTile;
+
+template <class T, class In, class Out>
+__global__ void __launch_bounds__(kSmallScanThreads) scan_small_k(In in, Out out, uint64_t count, T* total) {
+  __shared__ T sm[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T carry = 0;
+  for (uint64_t t0 = 0; t0 < count; t0 += kSmallScanTile) {
+    const uint64_t sub = t0 + static_cast<uint64_t>(warp) * (32 * kScanItems);
+    T vals[kScanItems];
+    T acc = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      const uint64_t i = sub + j * 32 + lane;
+      vals[j] = i < count ? in(i) : T(0);
+      acc += vals[j];
+    }
+    const T wtot = warp_sum(acc);
+    T tot;
+    T pre = block_exclusive_scan<T>(lane == 0 ? wtot : T(0), sm, tot);
+    pre = __shfl_sync(0xffffffffu, pre, 0) + carry;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      const T inc = warp_inclusive_scan(vals[j]);
+      const uint64_t i = sub + j * 32 + lane;
+      if (i < count) out(i, pre + inc - vals[j]);
+      pre += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
 // Exclusive scan of in(0..count) delivered to out(i, prefix); the grand total
 // lands in *total_dev (device pointer, may be null).  No host sync.
 template <class T, class In, class Out>
 void device_scan(gbg_graph* g, In in, Out out, uint64_t count, T* total_dev, const char* tag = "scan") {
+  if (count <= kSmallScan) {
+    GBG_LAUNCH(g, (scan_small_k<T, In, Out>), 1, kSmallScanThreads, 0, in, out, count, total_dev);
+    return;
+  }
   uint64_t nb = (count + kScanTile - 1) / kScanTile;
   if (nb == 0) nb = 1;
   T* sums = g->ws.get<T>(std::string(tag) + ".sums", nb);
