@@ -113,6 +113,139 @@ static __global__ void __launch_bounds__(kSortThreads, 2) onesweep_ballot_k(cons
   }
 }
 
+
+// ---- variant v2: tile keys staged in shared memory by a 1-D bulk copy,
+// ballot ranking, two shared buffers (in / digit-ordered out), 3 CTAs per
+// SM, look-back reading 4 predecessor states at once.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+template <int kRounds>
+static __global__ void __launch_bounds__(kSortThreads, 3) onesweep_v2_k(const uint64_t* __restrict__ in,
+                                                                       uint64_t* __restrict__ out, uint64_t n,
+                                                                       int shift, const uint32_t* __restrict__ base,
+                                                                       uint64_t* state, unsigned int* tile_ctr) {
+  constexpr int kWarps = kSortThreads / 32;
+  constexpr uint32_t kTile = kSortThreads * kRounds;
+  constexpr uint32_t kSub = kTile / kWarps;
+  extern __shared__ __align__(16) uint64_t s_dyn[];
+  uint64_t* s_in = s_dyn;
+  uint64_t* s_out = s_dyn + kTile;
+  __shared__ uint32_t s_base[kRadix];
+  __shared__ uint32_t s_start[kRadix];
+  __shared__ uint32_t s_cnt[kWarps][kRadix];
+  __shared__ uint32_t s_red[33];
+  __shared__ uint32_t s_tile;
+  __shared__ __align__(8) uint64_t s_bar;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(tile_ctr, 1u);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (uint32_t x = lane; x < kRadix; x += 32) s_cnt[warp][x] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t tile0 = static_cast<uint64_t>(tile) * kTile;
+  const uint32_t len = static_cast<uint32_t>(n - tile0 < kTile ? n - tile0 : kTile);
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = len * 8;  // multiple of 8; bulk copies need 16: pad with one key below
+    const uint32_t b16 = (bytes + 15) & ~15u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&s_bar)), "r"(b16) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(s_in)),
+                 "l"(in + tile0), "r"(b16), "r"(smem_addr(&s_bar))
+                 : "memory");
+  }
+  {
+    uint32_t done;
+    do {
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+                   : "=r"(done)
+                   : "r"(smem_addr(&s_bar))
+                   : "memory");
+    } while (!done);
+  }
+  const uint32_t lt = (1u << lane) - 1;
+  const uint32_t w0 = warp * kSub;
+  uint32_t pm[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const uint32_t i = w0 + r * 32 + lane;
+    const bool valid = i < len;
+    const uint32_t d = static_cast<uint32_t>((s_in[i] >> shift) & (kRadix - 1));
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+      const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+    pm[r] = peers;
+    if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const uint32_t d = threadIdx.x;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) tot += s_cnt[w][d];
+    volatile uint64_t* st = state + static_cast<uint64_t>(tile) * kRadix + d;
+    *st = (tile == 0 ? kLbPre : kLbAgg) | tot;
+    uint32_t all;
+    const uint32_t start = block_exclusive_scan(tot, s_red, all);
+    s_start[d] = start;
+    uint32_t run = start;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_cnt[w][d];
+      s_cnt[w][d] = run;
+      run += c;
+    }
+    // look-back, 4 predecessor states per step
+    uint64_t excl = 0;
+    int64_t t = static_cast<int64_t>(tile) - 1;
+    while (t >= 0) {
+      uint64_t v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        v[q] = t - q >= 0 ? *(const volatile uint64_t*)(state + static_cast<uint64_t>(t - q) * kRadix + d) : kLbPre;
+      bool stop = false;
+      int q = 0;
+      for (; q < 4 && t - q >= 0; ++q) {
+        uint64_t x = v[q];
+        while ((x >> 62) == 0) x = *(const volatile uint64_t*)(state + static_cast<uint64_t>(t - q) * kRadix + d);
+        excl += x & kLbVal;
+        if ((x >> 62) == 2) {
+          stop = true;
+          break;
+        }
+      }
+      if (stop) break;
+      t -= 4;
+    }
+    if (tile > 0) *st = kLbPre | (excl + tot);
+    s_base[d] = base[d] + static_cast<uint32_t>(excl);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const uint32_t i = w0 + r * 32 + lane;
+    const bool valid = i < len;
+    const uint64_t key = s_in[i];
+    const uint32_t d = static_cast<uint32_t>((key >> shift) & (kRadix - 1));
+    const uint32_t peers = pm[r];
+    if (valid) s_out[s_cnt[warp][d] + __popc(peers & lt)] = key;
+    __syncwarp();
+    if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < len; j += kSortThreads) {
+    const uint64_t key = s_out[j];
+    const uint32_t d = static_cast<uint32_t>((key >> shift) & (kRadix - 1));
+    out[s_base[d] + (j - s_start[d])] = key;
+  }
+}
+
 #define CK(x)                                                                    \
   do {                                                                           \
     cudaError_t e_ = (x);                                                        \
@@ -193,6 +326,10 @@ int main(int argc, char** argv) {
   run("ballot ranking, 8 rounds", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
     onesweep_ballot_k<8><<<nt, kSortThreads>>>(a, b, n, sh, bs, d_state, d_ctr);
   }, kSortThreads * 8);
+  cudaFuncSetAttribute(onesweep_v2_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8);
+  run("v2: bulk-staged tile, ballot ranking, 3 CTAs/SM, 4-wide look-back", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
+    onesweep_v2_k<16><<<nt, kSortThreads, 2 * 4096 * 8>>>(a, b, n, sh, bs, d_state, d_ctr);
+  }, kSortThreads * 16);
   run("ballot, 16 rounds, NO look-back (timing only)", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
     onesweep_ballot_k<16, true><<<nt, kSortThreads>>>(a, b, n, sh, bs, d_state, d_ctr);
   }, kSortThreads * 16);
