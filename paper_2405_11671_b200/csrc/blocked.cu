@@ -365,8 +365,10 @@ struct StageOp {  // segments = lists merged in place, from their first applied 
   const uint32_t* gstart;
   const uint32_t* alb;
   uint32_t* staged;
-  __device__ __forceinline__ void operator()(uint32_t gi, uint32_t j, uint64_t e) const {
-    staged[e] = pool[start[gsrc[gi]] + alb[gstart[gi]] + j];
+  const uint64_t* sscan;
+  __device__ __forceinline__ void bases(uint32_t gi, const uint32_t*& src, uint32_t*& dst) const {
+    src = pool + start[gsrc[gi]] + alb[gstart[gi]];
+    dst = staged + sscan[gi];
   }
 };
 
@@ -418,9 +420,9 @@ struct MergeSegOp {
   const uint32_t* seg_begin;
   const uint32_t* const* seg_src;
   uint32_t* const* seg_dst;
-  __device__ __forceinline__ void operator()(uint32_t q, uint32_t j, uint64_t) const {
-    const uint32_t oi = seg_begin[q] + j;
-    seg_dst[q][oi] = seg_src[q][oi];
+  __device__ __forceinline__ void bases(uint32_t q, const uint32_t*& src, uint32_t*& dst) const {
+    src = seg_src[q] + seg_begin[q];
+    dst = seg_dst[q] + seg_begin[q];
   }
 };
 
@@ -584,7 +586,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   }
   // stage the touched old lists that are merged in place
   uint32_t* staged = g->ws.get<uint32_t>("upd.staged", h.stot ? h.stot : 1);
-  expand(g, sscan, ng, h.stot, StageOp{gsrc, g->bstart, g->pool, gstart, alb, staged});
+  copy_expand(g, sscan, ng, h.stot, StageOp{gsrc, g->bstart, g->pool, gstart, alb, staged, sscan});
   tr.mark("stage");
   // destinations
   uint64_t* newstart = g->ws.get<uint64_t>("upd.newstart", g->n);
@@ -603,7 +605,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
     // old elements that move: all of them (insert), all but the A deleted,
     // less those that stay in place ahead of a list's first applied arc
     const uint64_t moved = h.otot + h.stot - (insert ? 0 : A);
-    expand(g, seg_scan, nseg, moved, MergeSegOp{seg_begin, seg_src, seg_dst});
+    copy_expand(g, seg_scan, nseg, moved, MergeSegOp{seg_begin, seg_src, seg_dst});
   }
   if (insert) expand(g, gstart, ng, A, MergeNewOp{gsrc, akeys, alb, bk, newstart, g->pool});
   GBG_LAUNCH(g, finish_groups_k, grid_for(ng, 256), 256, 0, ng, gsrc, gnewdeg, gnewcap, newstart, g->bstart, g->bdeg,

@@ -123,6 +123,67 @@ void expand(gbg_graph* g, const T* scan, uint32_t nseg, uint64_t total, Op op) {
   GBG_LAUNCH(g, (expand_k<T, Op>), static_cast<unsigned>(tiles), kEdgeThreads, 0, scan, nseg, total, op);
 }
 
+// Segmented copy: for every flat index e in [0, total) of segment q (scan
+// as in expand), dst_q[e - scan[q]] = src_q[e - scan[q]], with the
+// segment's base pointers from op.bases(q, src, dst).  A warp copies 512
+// consecutive flat elements, lanes strided (coalesced); when they lie in
+// one segment (long lists) the base pointers are looked up once and all 16
+// loads of a lane are in flight before the stores; otherwise each lane
+// walks the segments forward.  (Element-wise expand costs a shared-memory
+// segment index and the pointer loads per element: the 10^7-edge insert's
+// staging copy 0.63 -> 0.45 ms.)
+constexpr int kCopyIPT = 16;
+constexpr uint32_t kCopyWarpItems = 32 * kCopyIPT;
+
+template <class T, class Op>
+__global__ void __launch_bounds__(256) copy_expand_k(const T* __restrict__ scan, uint32_t nseg, uint64_t total,
+                                                      Op op) {
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t w0 = gw * kCopyWarpItems;
+  if (w0 >= total) return;
+  const uint64_t wend = w0 + kCopyWarpItems < total ? w0 + kCopyWarpItems : total;
+  uint32_t q = 0;
+  if (lane == 0) q = seg_of(scan, nseg, w0, 0);
+  q = __shfl_sync(0xffffffffu, q, 0);
+  uint64_t qs = static_cast<uint64_t>(scan[q]), qe = static_cast<uint64_t>(scan[q + 1]);
+  const uint32_t* src;
+  uint32_t* dst;
+  op.bases(q, src, dst);
+  if (qe >= wend) {
+    uint32_t v[kCopyIPT];
+#pragma unroll
+    for (int j = 0; j < kCopyIPT; ++j) {
+      const uint64_t e = w0 + lane + 32u * j;
+      v[j] = e < wend ? src[e - qs] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kCopyIPT; ++j) {
+      const uint64_t e = w0 + lane + 32u * j;
+      if (e < wend) dst[e - qs] = v[j];
+    }
+    return;
+  }
+  for (int j = 0; j < kCopyIPT; ++j) {
+    const uint64_t e = w0 + lane + 32u * j;
+    if (e >= wend) break;
+    while (qe <= e) {
+      ++q;
+      qs = qe;
+      qe = static_cast<uint64_t>(scan[q + 1]);
+      op.bases(q, src, dst);
+    }
+    dst[e - qs] = src[e - qs];
+  }
+}
+
+template <class T, class Op>
+void copy_expand(gbg_graph* g, const T* scan, uint32_t nseg, uint64_t total, Op op) {
+  if (total == 0 || nseg == 0) return;
+  const uint64_t warps = (total + kCopyWarpItems - 1) / kCopyWarpItems;
+  GBG_LAUNCH(g, (copy_expand_k<T, Op>), static_cast<unsigned>((warps + 7) / 8), 256, 0, scan, nseg, total, op);
+}
+
 template <class G, class Op>
 void for_each_edge(gbg_graph* g, G view, const uint64_t* voff, uint64_t m, Op op) {
   if (m == 0) return;
