@@ -99,7 +99,7 @@ constexpr uint32_t kMinTilesPerSm = GBG_PR_MIN_TILES_PER_SM;
 #endif
 constexpr int kPrThreads = GBG_PR_THREADS;
 // Fixed-point scale of the row sums: 2^F, F = ceil(log2(m)) + kFixMargin
-// (at most 62; 62 below 2^26 arcs).  A contrib is about 1/m of the rank
+// (at most 62; 62 up to 2^22 arcs).  A contrib is about 1/m of the rank
 // mass (PageRank of an undirected graph is close to degree / 2m), so its
 // rounding error relative to its size is ~2^-kFixMargin at every scale:
 // measured 5.8e-11 / 6.1e-11 relative L1 after 20 iterations at scales 22 /
@@ -112,12 +112,15 @@ constexpr int kPrThreads = GBG_PR_THREADS;
 #define GBG_PR_FIX_MARGIN 28
 #endif
 constexpr int kFixMargin = GBG_PR_FIX_MARGIN;
+#ifndef GBG_PR_FIX_FLOOR_LG
+#define GBG_PR_FIX_FLOOR_LG 22
+#endif
 inline int fix_bits_for(uint64_t m) {
   int lg = 0;  // ceil(log2(m))
   while ((uint64_t{1} << lg) < m) ++lg;
-  // below 2^26 arcs the finest scale: small graphs keep ~1e-13 sums
+  // up to 2^22 arcs the finest scale: small graphs keep ~1e-13 sums
   // (equal-contrib graphs such as K_n round every term the same way)
-  return lg <= 26 ? 62 : std::min(62, lg + kFixMargin);
+  return lg <= GBG_PR_FIX_FLOOR_LG ? 62 : std::min(62, lg + kFixMargin);
 }
 
 // One staged chunk of a tile: arcs [e0, e0 + len), work groups [g0, g0 +
@@ -458,11 +461,16 @@ void layout_finish(gbg_graph* g, PrLayout* L) {
   // 3. blocks and tiles
   uint64_t* block_arc = g->ws.get<uint64_t>("prl.blockarc", L->nblocks);
   GBG_LAUNCH(g, block_starts_k, grid_for(nruns, 256), 256, 0, k, run_off, nruns, shift, block_arc);
-  // tiles of up to kTileArcs arcs, smaller on small graphs so that there
-  // are at least kMinTilesPerSm tiles per SM to balance over
+  // tiles of up to kTileArcs arcs, smaller on smaller graphs so that there
+  // are at least kMinTilesPerSm tiles per SM to balance over, but not below
+  // 2^17 arcs (measured: s24 best at 2^19, s22 and s20 at 2^17 -- s20 1.99
+  // -> 1.79 ms against 2^16)
   int tile_bits = 0;
   while ((2ull << tile_bits) <= kTileArcs) ++tile_bits;
-  while (tile_bits > 16 && (m >> tile_bits) < uint64_t{kMinTilesPerSm} * g->sm_count) --tile_bits;
+  while (tile_bits > 17 && (m >> tile_bits) < uint64_t{kMinTilesPerSm} * g->sm_count) --tile_bits;
+#ifdef GBG_PR_TILE_BITS_FORCE
+  tile_bits = GBG_PR_TILE_BITS_FORCE;
+#endif
   TileIn tin{k, run_off, block_arc, shift, tile_bits};
   device_scan<uint32_t>(g, tin, NullOut{}, nruns, cnt + 1, "prl.tiles");
   read_scalars(g, cnt + 1, sizeof(uint32_t), &L->ntiles);

@@ -132,6 +132,77 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_k(In in, Out out, uint
   }
 }
 
+// Single-pass scan (decoupled look-back): tiles in processing order from
+// an atomic counter; a tile publishes its aggregate as soon as it has
+// summed its items, then warp 0 looks back over the preceding tiles' states
+// 32 at a time (lane k reads tile t-1-k) until it finds an inclusive
+// prefix, and the tile publishes its own.  The inputs are read once (the
+// reduce-then-scan form reads them twice).  State word: flag in the top 2
+// bits (1 = aggregate, 2 = inclusive prefix), value below.
+constexpr uint64_t kScanAgg = 1ull << 62, kScanPre = 2ull << 62, kScanVal = (1ull << 62) - 1;
+
+template <class T, class In, class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_onepass_k(In in, Out out, uint64_t count, uint64_t* state,
+                                                              unsigned* tile_ctr, T* total) {
+  __shared__ T sm[33];
+  __shared__ uint32_t s_tile;
+  __shared__ T s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t sub = static_cast<uint64_t>(tile) * kScanTile + static_cast<uint64_t>(warp) * (32 * kScanItems);
+  T vals[kScanItems];
+  T acc = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const uint64_t i = sub + j * 32 + lane;
+    vals[j] = i < count ? in(i) : T(0);
+    acc += vals[j];
+  }
+  const T wtot = warp_sum(acc);
+  T tot;
+  T pre = block_exclusive_scan<T>(lane == 0 ? wtot : T(0), sm, tot);
+  if (warp == 0) {
+    volatile uint64_t* st = state + tile;
+    if (lane == 0) *st = (tile == 0 ? kScanPre : kScanAgg) | static_cast<uint64_t>(tot);
+    uint64_t excl = 0;
+    if (tile > 0) {
+      int64_t t = static_cast<int64_t>(tile) - 1;
+      for (;;) {
+        const int64_t mine = t - lane;
+        uint64_t v = mine >= 0 ? *(const volatile uint64_t*)(state + mine) : kScanPre;
+        uint32_t need, pre_m;
+        for (;;) {  // every state up to the nearest published prefix must be in
+          pre_m = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+          need = pre_m ? (2u << (__ffs(pre_m) - 1)) - 1u : 0xffffffffu;
+          if ((__ballot_sync(0xffffffffu, (v >> 62) == 0) & need) == 0) break;
+          if ((v >> 62) == 0) v = *(const volatile uint64_t*)(state + mine);
+        }
+        uint64_t add = ((need >> lane) & 1u) ? (v & kScanVal) : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) add += __shfl_xor_sync(0xffffffffu, add, d);
+        excl += add;
+        if (pre_m) break;
+        t -= 32;
+      }
+      if (lane == 0) *st = kScanPre | (excl + static_cast<uint64_t>(tot));
+    }
+    if (lane == 0) s_excl = static_cast<T>(excl);
+  }
+  __syncthreads();
+  pre = __shfl_sync(0xffffffffu, pre, 0) + s_excl;
+  if (threadIdx.x == 0 && total && (static_cast<uint64_t>(tile) + 1) * kScanTile >= count)
+    *total = s_excl + tot;  // the last tile
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const T inc = warp_inclusive_scan(vals[j]);
+    const uint64_t i = sub + j * 32 + lane;
+    if (i < count) out(i, pre + inc - vals[j]);
+    pre += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
 // Small scans (count <= kSmallScan): one CTA of 1024 threads walks the
 // items in tiles of 16K (same warp-striped rounds as scan_down_k) and
 // carries the running prefix -- one launch instead of three, for the
@@ -179,6 +250,17 @@ void device_scan(gbg_graph* g, In in, Out out, uint64_t count, T* total_dev, con
     GBG_LAUNCH(g, (scan_small_k<T, In, Out>), 1, kSmallScanThreads, 0, in, out, count, total_dev);
     return;
   }
+#ifndef GBG_SCAN_TWO_PASS
+  {
+    const uint64_t nt = (count + kScanTile - 1) / kScanTile;
+    uint64_t* st = g->ws.get<uint64_t>(std::string(tag) + ".lb", nt + 1);
+    unsigned* ctr = reinterpret_cast<unsigned*>(st + nt);
+    GBG_CUDA(cudaMemsetAsync(st, 0, (nt + 1) * sizeof(uint64_t), g->stream));
+    GBG_LAUNCH(g, (scan_onepass_k<T, In, Out>), static_cast<unsigned>(nt), kScanThreads, 0, in, out, count, st, ctr,
+               total_dev);
+    return;
+  }
+#endif
   uint64_t nb = (count + kScanTile - 1) / kScanTile;
   if (nb == 0) nb = 1;
   T* sums = g->ws.get<T>(std::string(tag) + ".sums", nb);
