@@ -108,6 +108,9 @@ constexpr int kPrThreads = GBG_PR_THREADS;
 // high word of a row sum only takes the carries out of the low word (a few
 // percent of the adds), and the high-word add is skipped when there is
 // none.  Row sums stay below 2^(64-F) >= 4.
+#ifndef GBG_PR_FIN_PREFETCH
+#define GBG_PR_FIN_PREFETCH 1
+#endif
 #ifndef GBG_PR_FIX_MARGIN
 #define GBG_PR_FIX_MARGIN 28
 #endif
@@ -840,6 +843,17 @@ __global__ void __launch_bounds__(kPrThreads, 1) pr_tile_k(PrArgs a) {
           break;
         }
         const PrChunk ch = nx;
+#if GBG_PR_FIN_PREFETCH
+        if ((ch.flags & (1u << 8)) && !(ch.flags & (1u << 10))) {
+          // the first chunk of a single-tile block: pull the block's degrees
+          // and previous contribs (read by its finalize) into L2
+          const uint32_t row0 = ch.block * kRows;
+          const uint32_t nrows = min(kRows, a.nz - row0);
+          const uint32_t bd = (nrows * 4u) & ~15u, bx = (nrows * 8u) & ~15u;
+          if (bd) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.deg + row0), "r"(bd) : "memory");
+          if (bx) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x_old + row0), "r"(bx) : "memory");
+        }
+#endif
         uint16_t* arcb;
         uint32_t* runb;
         uint32_t* grpb;
