@@ -546,18 +546,6 @@ struct MergeSegOp {
   }
 };
 
-// inserted arc r of group gi -> slot r + (old neighbours below it)
-struct MergeNewOp {
-  const uint32_t* gsrc;
-  const uint64_t* akeys;
-  const uint32_t* alb;
-  BatchKeys bk;
-  const uint64_t* newstart;
-  uint32_t* pool;
-  __device__ __forceinline__ void operator()(uint32_t gi, uint32_t r, uint64_t i) const {
-    pool[newstart[gsrc[gi]] + r + alb[i]] = bk.dst(akeys[i]);
-  }
-};
 
 // destination of each touched list: in place, or a fresh bump allocation
 __global__ void plan_dest_k(uint32_t ng, const uint32_t* gsrc, const uint64_t* galloc_scan, const uint64_t* galloc,

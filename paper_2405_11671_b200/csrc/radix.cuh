@@ -65,8 +65,9 @@ static __global__ void __launch_bounds__(kSortThreads) radix_bases_k(uint32_t* h
   }
 }
 
-template <bool kReload>
-static __global__ void __launch_bounds__(kSortThreads, kReload ? 4 : 3) radix_onesweep_k(const uint64_t* __restrict__ in,
+// the register-resident pass: only for sorts the small path cannot take
+// (n <= kSmallMax with more than 51 key bits)
+static __global__ void __launch_bounds__(kSortThreads, 3) radix_onesweep_k(const uint64_t* __restrict__ in,
                                                                         uint64_t* __restrict__ out, uint64_t n,
                                                                         int shift, const uint32_t* __restrict__ base,
                                                                         uint64_t* state, unsigned int* tile_ctr) {
@@ -85,29 +86,16 @@ static __global__ void __launch_bounds__(kSortThreads, kReload ? 4 : 3) radix_on
   const uint32_t tile = s_tile;
   const uint64_t base0 = static_cast<uint64_t>(tile) * kSortTile + static_cast<uint64_t>(warp) * kSub;
   const uint32_t lt = (1u << lane) - 1;
-  // 1. each warp: its keys (coalesced) and digit counts.  kReload (large
-  // sorts): the peer masks (lanes of the round with the same digit) are
-  // kept for the ranking and the digits as bytes, and the keys are read
-  // again (L2) for the scatter instead of held in 32 registers -- one
-  // match_any per key instead of two, at 64 registers (4 CTAs per SM).
-  // Otherwise (small sorts, latency-bound) the keys stay in registers.
-  uint32_t pm[kSortRounds];
-  uint32_t dg[kSortRounds / 4];  // four 8-bit digits per word
-  uint64_t k[kReload ? 1 : kSortRounds];
-#pragma unroll
-  for (int r = 0; r < kSortRounds / 4; ++r) dg[r] = 0;
+  // 1. each warp: its keys (coalesced) and digit counts
+  uint64_t k[kSortRounds];
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
     const uint64_t i = base0 + r * 32 + lane;
     const bool valid = i < n;
     const uint64_t key = valid ? in[i] : ~0ull;
-    if (!kReload) k[r] = key;
+    k[r] = key;
     const uint32_t d = valid ? static_cast<uint32_t>((key >> shift) & (kRadix - 1)) : kRadix + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    if (kReload) {
-      pm[r] = peers;
-      dg[r / 4] |= (d & 0xffu) << (8 * (r % 4));
-    }
     if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
     __syncwarp();
   }
@@ -153,15 +141,9 @@ static __global__ void __launch_bounds__(kSortThreads, kReload ? 4 : 3) radix_on
   for (int r = 0; r < kSortRounds; ++r) {
     const uint64_t i = base0 + r * 32 + lane;
     const bool valid = i < n;
-    uint32_t d, peers;
-    if (kReload) {
-      d = (dg[r / 4] >> (8 * (r % 4))) & 0xffu;
-      peers = pm[r];
-    } else {
-      d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
-      peers = __match_any_sync(0xffffffffu, d);
-    }
-    if (valid) s_keys[s_cnt[warp][d] + __popc(peers & lt)] = kReload ? in[i] : k[r];
+    const uint32_t d = valid ? static_cast<uint32_t>((k[r] >> shift) & (kRadix - 1)) : kRadix + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (valid) s_keys[s_cnt[warp][d] + __popc(peers & lt)] = k[r];
     __syncwarp();
     if (valid && (peers & lt) == 0) s_cnt[warp][d] += __popc(peers);
     __syncwarp();
@@ -178,7 +160,7 @@ static __global__ void __launch_bounds__(kSortThreads, kReload ? 4 : 3) radix_on
   }
 }
 
-// Large sorts (n > 2^20): the same pass with the tile staged in shared
+// Sorts above the small path: the same pass with the tile staged in shared
 // memory by one 1-D bulk copy (no key registers: 3 CTAs per SM), in-warp
 // ranking by bit-sliced ballots (eight votes give each key the mask of the
 // round's lanes with its digit), the digit-ordered tile in a second shared
@@ -189,6 +171,9 @@ __device__ __forceinline__ uint32_t radix_smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 constexpr size_t kSortBulkSmem = 2ull * kSortTile * sizeof(uint64_t);
+#ifndef GBG_SORT_BULK_MIN
+#define GBG_SORT_BULK_MIN 0  // every sort above the small path (10^5-edge batch: 0.76 -> 0.71 ms)
+#endif
 
 static __global__ void __launch_bounds__(kSortThreads, 3) radix_onesweep_bulk_k(
     const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t n, int shift,
@@ -423,12 +408,12 @@ inline uint64_t* radix_sort_u64(gbg_graph* g, uint64_t* keys, uint64_t* scratch,
   uint64_t* dst = scratch;
   for (int p = 0; p < passes; ++p) {
     GBG_CUDA(cudaMemsetAsync(state, 0, static_cast<uint64_t>(ntiles) * kRadix * sizeof(uint64_t), g->stream));
-    if (n > (1u << 20))
+    if (n > GBG_SORT_BULK_MIN)
       GBG_LAUNCH(g, radix_onesweep_bulk_k, ntiles, kSortThreads, kSortBulkSmem, src, dst, n, p * kRadixBits,
                  hist + p * kRadix,
                  state, ctr + p);
     else
-      GBG_LAUNCH(g, radix_onesweep_k<false>, ntiles, kSortThreads, 0, src, dst, n, p * kRadixBits, hist + p * kRadix,
+      GBG_LAUNCH(g, radix_onesweep_k, ntiles, kSortThreads, 0, src, dst, n, p * kRadixBits, hist + p * kRadix,
                  state, ctr + p);
     std::swap(src, dst);
   }

@@ -1,6 +1,7 @@
 // Stand-alone timing of one LSD radix pass over uint64 keys (analysis only):
-// the library's onesweep pass (radix.cuh) against a variant whose in-warp
-// ranking uses bit-sliced ballots instead of __match_any_sync.
+// the library's onesweep passes (radix.cuh) against the experimental
+// variants that led to the bulk-staged pass (ballot ranking; v2 = what
+// radix_onesweep_bulk_k now is).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2405_11671_b200/csrc \
 //        profiles/sort_bench.cu -o profiles/sort_bench
 #include <cstdio>
@@ -314,11 +315,12 @@ int main(int argc, char** argv) {
     }
     printf("%s: pass %.1f us = %.2f TB/s (read+write)\n", name, best * 1e3, 16.0 * n / (best * 1e-3) / 1e12);
   };
-  run("library onesweep<reload>", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
-    radix_onesweep_k<true><<<nt, kSortThreads>>>(a, b, n, sh, bs, d_state, d_ctr);
+  run("library onesweep (small sorts: match_any, keys in registers)", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
+    radix_onesweep_k<<<nt, kSortThreads>>>(a, b, n, sh, bs, d_state, d_ctr);
   }, kSortTile);
-  run("library onesweep<regs>", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
-    radix_onesweep_k<false><<<nt, kSortThreads>>>(a, b, n, sh, bs, d_state, d_ctr);
+  cudaFuncSetAttribute(radix_onesweep_bulk_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortBulkSmem);
+  run("library onesweep (large sorts: bulk-staged tile, ballot ranking)", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
+    radix_onesweep_bulk_k<<<nt, kSortThreads, kSortBulkSmem>>>(a, b, n, sh, bs, d_state, d_ctr);
   }, kSortTile);
   run("ballot ranking, 16 rounds", [&](uint32_t nt, uint64_t* a, uint64_t* b, int sh, const uint32_t* bs) {
     onesweep_ballot_k<16><<<nt, kSortThreads>>>(a, b, n, sh, bs, d_state, d_ctr);
