@@ -214,23 +214,31 @@ __device__ __forceinline__ uint32_t gallop_lb(const uint32_t* lst, uint32_t len,
 __device__ __forceinline__ uint64_t sym_hash(uint64_t key, uint64_t salt) { return mix64(key * 0x9e3779b97f4a7c15ull + salt); }
 // kFlagArcs = 1 for small batches, where the chain of searches of one
 // thread would be the critical path
+// The sorted raw keys go in directly: a duplicate of the previous key or a
+// self-loop (the dropped-key sentinel included) is not applied -- the
+// unique step of prepare (batch.cpp:34-42) folded into this pass, one
+// scan less; U counts the unique arcs.
 template <int kFlagArcs>
-__global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t* U_dev, BatchKeys bk,
+__global__ void apply_flags_k(const uint64_t* k, uint64_t count, unsigned long long* U_dev, BatchKeys bk,
                               const uint64_t* start, const uint32_t* deg, const uint32_t* pool, int insert,
                               uint32_t* flag, uint32_t* lb, int check_sym, unsigned long long* hsum, uint64_t* lt,
                               uint64_t* gt) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kFlagArcs;
-  const uint64_t U = *U_dev;
-  uint32_t nlt = 0, ngt = 0;
+  uint32_t nlt = 0, ngt = 0, nu = 0;
   unsigned long long h1 = 0, h2 = 0;
-  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kFlagArcs; i0 < U; i0 += stride) {
+  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kFlagArcs; i0 < count; i0 += stride) {
     uint32_t ps = ~0u, ppos = 0;
 #pragma unroll
     for (int j = 0; j < kFlagArcs; ++j) {
       const uint64_t i = i0 + j;
-      if (i >= U) break;
+      if (i >= count) break;
       const uint64_t x = k[i];
       const uint32_t s = bk.src(x), d = bk.dst(x);
+      if ((i > 0 && k[i - 1] == x) || s == d) {
+        flag[i] = 0;
+        continue;
+      }
+      ++nu;
       const uint32_t* lst = pool + start[s];
       const uint32_t len = deg[s];
       const uint32_t pos = s == ps ? gallop_lb(lst, len, d, ppos) : lower_bound_u32(lst, len, d);
@@ -253,6 +261,8 @@ __global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t*
       }
     }
   }
+  nu = __reduce_add_sync(0xffffffffu, nu);
+  if ((threadIdx.x & 31) == 0 && nu) atomicAdd(U_dev, static_cast<unsigned long long>(nu));
   if (check_sym) {
     nlt = __reduce_add_sync(0xffffffffu, nlt);
     ngt = __reduce_add_sync(0xffffffffu, ngt);
@@ -268,13 +278,12 @@ __global__ void apply_flags_k(const uint64_t* k, uint64_t count, const uint64_t*
 }
 struct ApplyOut {
   const uint32_t* flag;
-  const uint64_t* U;
   const uint64_t* k;
   const uint32_t* lb;
   uint64_t* out;
   uint32_t* out_lb;
   __device__ __forceinline__ void operator()(uint64_t i, uint32_t pre) const {
-    if (i < *U && flag[i]) {
+    if (flag[i]) {
       out[pre] = k[i];
       out_lb[pre] = lb[i];
     }
@@ -639,24 +648,23 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint64_t* sorted = g->ws.get<uint64_t>("upd.sorted", count);
   GBG_LAUNCH(g, make_keys_k, grid_for(count, 256), 256, 0, pairs_dev, count, g->n, bk, keys, &sc->bad);
   uint64_t* srt = radix_sort_u64(g, keys, sorted, count, 2 * bk.L, "upd");
-  uint64_t* ukeys = srt == keys ? sorted : keys;
-  device_scan<uint64_t>(g, UniqueIn{srt, bk}, UniqueOut{srt, bk, ukeys}, count, &sc->U, "upd.uniq");
-  uint64_t* akeys = srt;  // free again: receives the applied arcs
+  uint64_t* akeys = srt == keys ? sorted : keys;  // receives the applied arcs
   tr.mark("prepare");
   // presence of each unique arc -> the applied arcs and their merge slots
   uint32_t* flag = g->ws.get<uint32_t>("upd.flag", count);
   uint32_t* lb = g->ws.get<uint32_t>("upd.lb", count);
   uint32_t* alb = g->ws.get<uint32_t>("upd.alb", count);
   if (count >= (1u << 21))
-    GBG_LAUNCH(g, apply_flags_k<4>, grid_for(count / 4 + 1, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk,
+    GBG_LAUNCH(g, apply_flags_k<4>, grid_for(count / 4 + 1, 256, g->sm_count * 16), 256, 0, srt, count,
+               reinterpret_cast<unsigned long long*>(&sc->U), bk,
                g->bstart, g->bdeg, g->pool, insert ? 1 : 0, flag, lb, g->symmetric ? 1 : 0, sc->hsum, &sc->lt,
                &sc->gt);
   else
-    GBG_LAUNCH(g, apply_flags_k<1>, grid_for(count, 256, g->sm_count * 16), 256, 0, ukeys, count, &sc->U, bk,
+    GBG_LAUNCH(g, apply_flags_k<1>, grid_for(count, 256, g->sm_count * 16), 256, 0, srt, count,
+               reinterpret_cast<unsigned long long*>(&sc->U), bk,
                g->bstart, g->bdeg, g->pool, insert ? 1 : 0, flag, lb, g->symmetric ? 1 : 0, sc->hsum, &sc->lt,
                &sc->gt);
-  device_scan<uint32_t>(g, BoundedIn<uint32_t, uint64_t>{flag, &sc->U}, ApplyOut{flag, &sc->U, ukeys, lb, akeys, alb},
-                        count, &sc->A, "upd.apply");
+  device_scan<uint32_t>(g, ArrayIn<uint32_t>{flag}, ApplyOut{flag, srt, lb, akeys, alb}, count, &sc->A, "upd.apply");
   // groups by source
   uint32_t* gstart = g->ws.get<uint32_t>("upd.gstart", count + 1);
   uint32_t* gsrc = g->ws.get<uint32_t>("upd.gsrc", count);
