@@ -603,7 +603,6 @@ struct BoundedOut {  // writes [0, n]: the exclusive prefix at n is the total (s
 struct UpdScalars {
   uint64_t U;     // unique, self-loop-free arcs (prepare)
   uint64_t need;  // pool ids the grown lists allocate
-  uint64_t otot;  // old elements of the touched lists that grow (merged from the pool)
   uint64_t mtot;  // old elements that may move (grown lists: all; in place: from the first applied arc)
   uint64_t stot;  // old elements staged: lists merged in place, from their first applied arc on
   uint32_t A;     // applied arcs
@@ -678,12 +677,17 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   uint64_t* galloc = g->ws.get<uint64_t>("upd.galloc", count);
   uint64_t* gascan = g->ws.get<uint64_t>("upd.gascan", count + 1);
   plan_allocations(g, count, gstart, gsrc, insert, sc, gcnt, gnewdeg, gnewcap, galloc, gascan);
-  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 0}, NullOut{}, count + 1,
-                        &sc->otot, "upd.oscan");
+  // mscan: every old element that may move (grown list: all d; merged in
+  // place: its staged tail), sscan: the staged tails alone
   uint64_t* mscan = g->ws.get<uint64_t>("upd.mscan", count + 1);
   uint64_t* sscan = g->ws.get<uint64_t>("upd.sscan", count + 1);
-  device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 1},
-                        BoundedOut<uint64_t, uint32_t>{sscan, &sc->ng}, count + 1, &sc->stot, "upd.sscan");
+  auto scan_moves = [&] {
+    device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 2},
+                          BoundedOut<uint64_t, uint32_t>{mscan, &sc->ng}, count + 1, &sc->mtot, "upd.mscan");
+    device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 1},
+                          BoundedOut<uint64_t, uint32_t>{sscan, &sc->ng}, count + 1, &sc->stot, "upd.sscan");
+  };
+  scan_moves();
   UpdScalars h;
   read_scalars(g, sc, sizeof(h), &h);
   tr.mark("plan");
@@ -697,8 +701,7 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
     GBG_LAUNCH(g, refresh_caps_k, grid_for(g->n, 256), 256, 0, g->n, g->bdeg, g->bcap);
     blocked_relayout(g, g->bstart, g->pool, 2 * h.need, true);
     plan_allocations(g, count, gstart, gsrc, insert, sc, gcnt, gnewdeg, gnewcap, galloc, gascan);
-    device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 1},
-                          BoundedOut<uint64_t, uint32_t>{sscan, &sc->ng}, count + 1, &sc->stot, "upd.sscan");
+    scan_moves();
     read_scalars(g, sc, sizeof(h), &h);
     if (g->pool_top + h.need > g->pool_cap) fail(GBG_ERR_OOM, "blocked pool exhausted after compaction");
   }
@@ -723,16 +726,12 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
                           "upd.segs");
     // old elements that move: all of them (insert), all but the A deleted,
     // less those that stay in place ahead of a list's first applied arc
-    const uint64_t moved = h.otot + h.stot - (insert ? 0 : A);
+    const uint64_t moved = h.mtot - (insert ? 0 : A);
     copy_expand(g, seg_scan, nseg, moved, MergeSegOp{seg_begin, seg_src, seg_dst});
   } else {
     // flat space of every old element that may move, then one warp per
     // 512 of them (group windows); the inserted arcs by a thread each
-    // (its total is otot + stot: grown lists move all d, lists merged in
-    // place their staged tails)
-    const uint64_t mtot = h.otot + h.stot;
-    device_scan<uint64_t>(g, OldDegIn{gsrc, g->bdeg, &sc->ng, galloc, gstart, alb, 2},
-                          BoundedOut<uint64_t, uint32_t>{mscan, &sc->ng}, count + 1, &sc->mtot, "upd.mscan");
+    const uint64_t mtot = h.mtot;
     if (mtot) {
       const uint64_t chunks = (mtot + kMergeChunk - 1) / kMergeChunk;
       uint32_t* first = g->ws.get<uint32_t>("upd.mfirst", chunks);
