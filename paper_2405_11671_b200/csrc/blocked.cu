@@ -691,6 +691,10 @@ uint64_t apply_batch(gbg_graph* g, const uint32_t* pairs_dev, uint64_t count, bo
   UpdScalars h;
   read_scalars(g, sc, sizeof(h), &h);
   tr.mark("plan");
+  if (PhaseTrace::enabled())
+    std::fprintf(stderr, "[gbg trace] batch: count %llu U %llu A %u ng %u need %llu mtot %llu stot %llu\n",
+                 (unsigned long long)count, (unsigned long long)h.U, h.A, h.ng, (unsigned long long)h.need,
+                 (unsigned long long)h.mtot, (unsigned long long)h.stot);
   if (h.bad) fail(GBG_ERR_OUT_OF_RANGE, "edge endpoint out of range");
   if (h.U == 0 || h.A == 0) return 0;
   if (h.under) fail(GBG_ERR_LOGIC, "metadata underflow: tracker and container diverged");

@@ -77,6 +77,26 @@ __device__ __forceinline__ uint32_t seg_of(const T* scan, uint32_t nseg, uint64_
   return lo;
 }
 
+// The same search by a whole warp (warp-uniform e): 32 probes per round
+// narrow [lo, hi) 32-fold, so ~log32(nseg) dependent loads instead of
+// log2(nseg) (a 34K-segment copy: 3 rounds instead of 15).
+template <class T>
+__device__ __forceinline__ uint32_t warp_seg_of(const T* scan, uint32_t nseg, uint64_t e) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = nseg;  // scan[lo] <= e < scan[hi]
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = lo + lane * step;
+    const bool le = idx < hi && static_cast<uint64_t>(scan[idx]) <= e;
+    const uint32_t mask = __ballot_sync(0xffffffffu, le);  // lane 0 always set
+    const uint32_t last = 31 - __clz(mask);
+    const uint32_t nlo = lo + last * step;
+    hi = nlo + step < hi ? nlo + step : hi;
+    lo = nlo;
+  }
+  return lo;
+}
+
 template <class T, class Op>
 __global__ void __launch_bounds__(kEdgeThreads) expand_k(const T* __restrict__ scan, uint32_t nseg, uint64_t total,
                                                           Op op) {
@@ -134,18 +154,23 @@ void expand(gbg_graph* g, const T* scan, uint32_t nseg, uint64_t total, Op op) {
 // staging copy 0.63 -> 0.45 ms.)
 constexpr int kCopyIPT = 16;
 constexpr uint32_t kCopyWarpItems = 32 * kCopyIPT;
+#ifndef GBG_COPY_MINB
+#define GBG_COPY_MINB 5
+#endif
+#ifndef GBG_COPY_WIN
+#define GBG_COPY_WIN 4
+#endif
+constexpr int kCopyWin = GBG_COPY_WIN;  // multi-segment chunks: elements per lane in flight
 
 template <class T, class Op>
-__global__ void __launch_bounds__(256) copy_expand_k(const T* __restrict__ scan, uint32_t nseg, uint64_t total,
+__global__ void __launch_bounds__(256, GBG_COPY_MINB) copy_expand_k(const T* __restrict__ scan, uint32_t nseg, uint64_t total,
                                                       Op op) {
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t w0 = gw * kCopyWarpItems;
   if (w0 >= total) return;
   const uint64_t wend = w0 + kCopyWarpItems < total ? w0 + kCopyWarpItems : total;
-  uint32_t q = 0;
-  if (lane == 0) q = seg_of(scan, nseg, w0, 0);
-  q = __shfl_sync(0xffffffffu, q, 0);
+  uint32_t q = warp_seg_of(scan, nseg, w0);
   uint64_t qs = static_cast<uint64_t>(scan[q]), qe = static_cast<uint64_t>(scan[q + 1]);
   const uint32_t* src;
   uint32_t* dst;
@@ -164,16 +189,52 @@ __global__ void __launch_bounds__(256) copy_expand_k(const T* __restrict__ scan,
     }
     return;
   }
-  for (int j = 0; j < kCopyIPT; ++j) {
-    const uint64_t e = w0 + lane + 32u * j;
-    if (e >= wend) break;
-    while (qe <= e) {
-      ++q;
-      qs = qe;
-      qe = static_cast<uint64_t>(scan[q + 1]);
-      op.bases(q, src, dst);
+  // several segments (short lists): windows of 32 segments, lane i holding
+  // segment qa + i's flat start and base pointers (one parallel load round);
+  // each element finds its segment by a 5-step shuffle search over the
+  // window (a lane walking the segments one by one paid a dependent chain
+  // of scan + pointer loads per segment)
+  for (uint32_t qa = q;; qa += 32) {
+    const uint32_t qi = qa + lane;
+    uint64_t si = total;
+    const uint32_t* srci = nullptr;
+    uint32_t* dsti = nullptr;
+    if (qi < nseg) {
+      si = static_cast<uint64_t>(scan[qi]);
+      op.bases(qi, srci, dsti);
     }
-    dst[e - qs] = src[e - qs];
+    const uint64_t wlo = __shfl_sync(0xffffffffu, si, 0);
+    const uint64_t whi = qa + 32 < nseg ? static_cast<uint64_t>(scan[qa + 32]) : total;  // warp-uniform
+    for (int h = 0; h < kCopyIPT; h += kCopyWin) {  // kCopyWin elements at a time (registers)
+      uint32_t v[kCopyWin];
+      uint32_t kk[kCopyWin];
+#pragma unroll
+      for (int j = 0; j < kCopyWin; ++j) {
+        const uint64_t e = w0 + lane + 32u * (h + j);
+        const bool in = e < wend && e >= wlo && e < whi;
+        uint32_t k = 0;
+#pragma unroll
+        for (uint32_t st = 16; st; st >>= 1) {
+          const uint64_t sk = __shfl_sync(0xffffffffu, si, k + st);
+          if (sk <= e) k += st;
+        }
+        const uint64_t sk = __shfl_sync(0xffffffffu, si, k);
+        const uint32_t* sp = reinterpret_cast<const uint32_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(srci), k));
+        kk[j] = k;
+        v[j] = in ? sp[e - sk] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kCopyWin; ++j) {
+        const uint64_t e = w0 + lane + 32u * (h + j);
+        const bool in = e < wend && e >= wlo && e < whi;
+        const uint64_t sk = __shfl_sync(0xffffffffu, si, kk[j]);
+        uint32_t* dp = reinterpret_cast<uint32_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dsti), kk[j]));
+        if (in) dp[e - sk] = v[j];
+      }
+    }
+    if (whi >= wend) break;
   }
 }
 
