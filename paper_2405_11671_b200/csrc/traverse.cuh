@@ -396,21 +396,29 @@ __device__ __forceinline__ bool pull_vertex(G g, const uint32_t* fb, Op op, cons
   return found;
 }
 
+// Word of a packed position: the largest k < kBatch with excl_k <= t, by a
+// binary search over the lanes' exclusive popcount prefixes (log2(kBatch)
+// shuffles).  Lanes past the batch hold excl == total > t, and an empty
+// word shares its prefix with the next one, so the word found is non-empty
+// for every t < total.
+template <uint32_t kBatch>
+__device__ __forceinline__ uint32_t packed_word(uint32_t excl, uint32_t t) {
+  uint32_t j = 0;
+#pragma unroll
+  for (uint32_t s = kBatch / 2; s > 0; s >>= 1) {
+    const uint32_t e = __shfl_sync(0xffffffffu, excl, j + s);
+    if (e <= t) j += s;
+  }
+  return j;
+}
+
 // Hand out the set bits of the lanes' words (lane k < B holds word wb + k
 // in `w`, exclusive prefix of the popcounts in `excl`) to the lanes: lane
 // t of round r0 gets bit number r0 + t; returns its word index j and bit.
-__device__ __forceinline__ void packed_bit(uint32_t w, uint32_t excl, uint32_t B, uint32_t t, uint32_t& j,
-                                           uint32_t& bit) {
-  uint32_t ej = 0;
-  j = 0;
-#pragma unroll
-  for (uint32_t k = 0; k < kCwBatch; ++k) {
-    const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
-    if (k < B && ek <= t) {
-      j = k;
-      ej = ek;
-    }
-  }
+template <uint32_t kBatch>
+__device__ __forceinline__ void packed_bit(uint32_t w, uint32_t excl, uint32_t t, uint32_t& j, uint32_t& bit) {
+  j = packed_word<kBatch>(excl, t);
+  const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
   const uint32_t wj = __shfl_sync(0xffffffffu, w, j);
   bit = __fns(wj, 0, static_cast<int>(t - ej + 1));
 }
@@ -426,13 +434,21 @@ __device__ __forceinline__ void packed_bit(uint32_t w, uint32_t excl, uint32_t B
 //    frontier-bit loads in flight at once; then the vertices that missed
 //    (18% at scale 24 level 1) packed onto the lanes, 32 per round, for
 //    the list scan from entry 1.
-// Each word's found bits are reassembled with warp OR-reductions; the
-// owning warp writes the output word and publishes the visited bits.
+// The level is issue-bound as much as latency-bound (ncu at scale 24 level
+// 1: 50% issue-slot use), so the per-word bookkeeping is kept off the
+// inner loops: found bits of the packed rounds are OR-ed into a per-warp
+// shared-memory word each (one ATOMS per round instead of a warp reduction
+// per word), the found count is the popcount of the finished words, and
+// per-batch bases replace 64-bit index arithmetic per word.  The owning
+// warp writes the output word and publishes the visited bits.
 template <class G, class Op>
 __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
                                               unsigned long long* packed, const uint64_t* fd,
                                               unsigned long long* examined, unsigned* heavy) {
+  __shared__ uint32_t s_fw[32][kCwBatch];  // found bits of the packed rounds, per warp and batch word
   const int lane = threadIdx.x & 31;
+  const uint32_t lbit = 1u << lane;
+  uint32_t* sf = s_fw[threadIdx.x >> 5];
   const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   // strided batches of B words (B <= kCwBatch): a warp's batches spread
@@ -442,11 +458,13 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
   const uint64_t per = (nwords + nwarps - 1) / nwarps;
   const uint32_t B = static_cast<uint32_t>(per < kCwBatch ? (per ? per : 1) : kCwBatch);
   unsigned long long cnt = 0, degsum = 0, ex = 0;
-  bool big = false;
+  uint32_t dmax = 0;
+  if (lane < static_cast<int>(kCwBatch)) sf[lane] = 0;
+  __syncwarp();
   for (uint64_t wb = gwarp * B; wb < nwords; wb += nwarps * B) {
     const uint64_t wend = wb + B < nwords ? wb + B : nwords;
     const uint64_t wl = wb + lane;
-    uint32_t cw = 0;
+    uint32_t cw = 0;  // lanes past the batch keep 0: their words have no live vertex
     if (wl < wend) {
       cw = op.cond_word(wl);
       if (wl * 32 + 32 > g.n) cw &= g.n > wl * 32 ? (1u << (g.n - wl * 32)) - 1u : 0u;
@@ -456,34 +474,37 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
     uint32_t total = __shfl_sync(0xffffffffu, excl + pc, 31);
     uint32_t fword = 0;  // lane k < B: found bits of word wb + k
     uint32_t todo = cw;  // lane k < B: live bits of word wb + k still to resolve
+    uint32_t exb = 0;
     bool first_done = false;
     if (total > 32) {
       // phase 1: first-neighbour tests, 4 words at a time
+      const uint32_t v0 = static_cast<uint32_t>(wb * 32) + lane;
+      const uint64_t* fdl = fd + wb * 32 + lane;
       uint32_t miss = 0;
-      for (uint32_t k0 = 0; k0 < B; k0 += kPh1) {
+#pragma unroll
+      for (uint32_t k0 = 0; k0 < kCwBatch; k0 += kPh1) {
+        if (k0 >= B) break;
         uint64_t x[kPh1];
         bool c[kPh1];
 #pragma unroll
         for (uint32_t q = 0; q < kPh1; ++q) {
-          c[q] = k0 + q < B && ((__shfl_sync(0xffffffffu, cw, (k0 + q) & 31) >> lane) & 1u);
-          x[q] = c[q] ? __ldg(fd + (wb + k0 + q) * 32 + lane) : 0ull;
+          c[q] = (__shfl_sync(0xffffffffu, cw, k0 + q) & lbit) != 0;
+          x[q] = c[q] ? __ldg(fdl + (k0 + q) * 32) : 0ull;
         }
         bool h[kPh1];
 #pragma unroll
-        for (uint32_t q = 0; q < kPh1; ++q) h[q] = c[q] && fd_deg(x[q]) && frontier_bit(fb, fd_first(x[q]));
+        for (uint32_t q = 0; q < kPh1; ++q) h[q] = fd_deg(x[q]) && frontier_bit(fb, fd_first(x[q]));
 #pragma unroll
         for (uint32_t q = 0; q < kPh1; ++q) {
-          const uint32_t v = static_cast<uint32_t>((wb + k0 + q) * 32 + lane);
-          const uint32_t d = fd_deg(x[q]);
-          if (h[q] && !op.update(fd_first(x[q]), v)) h[q] = false;
-          ex += c[q] && d ? 1 : 0;
+          const uint32_t d = fd_deg(x[q]);  // 0 for a lane without a live vertex
+          if (h[q] && !op.update(fd_first(x[q]), v0 + (k0 + q) * 32)) h[q] = false;
+          exb += d ? 1 : 0;
           if (h[q]) {
-            ++cnt;
             degsum += d;
-            big |= d > kBitmapPushMaxDeg;
+            dmax = max(dmax, d);
           }
           const uint32_t fm = __ballot_sync(0xffffffffu, h[q]);
-          const uint32_t mm = __ballot_sync(0xffffffffu, c[q] && !h[q] && d > 1);
+          const uint32_t mm = __ballot_sync(0xffffffffu, !h[q] && d > 1);
           if (lane == static_cast<int>(k0 + q)) {
             fword = fm;
             miss = mm;
@@ -501,31 +522,34 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
       const uint32_t t = r0 + lane;
       const bool c = t < total;
       uint32_t j, bit;
-      packed_bit(todo, excl, B, t, j, bit);
+      packed_bit<kCwBatch>(todo, excl, t, j, bit);
       if (!c) bit = 0;
       const uint32_t v = static_cast<uint32_t>((wb + j) * 32 + bit);
       uint32_t d;
       const bool found = first_done ? pull_vertex<false>(g, fb, op, fd, c, v, d, ex)
                                     : pull_vertex<true>(g, fb, op, fd, c, v, d, ex);
-      const uint32_t mine = found ? 1u << bit : 0u;
-#pragma unroll
-      for (uint32_t k = 0; k < kCwBatch; ++k) {
-        if (k >= B) break;
-        const uint32_t m = __reduce_or_sync(0xffffffffu, j == k ? mine : 0u);
-        if (lane == static_cast<int>(k)) fword |= m;
-      }
       if (found) {
-        ++cnt;
+        atomicOr(sf + j, 1u << bit);
         degsum += d;
-        big |= d > kBitmapPushMaxDeg;
+        dmax = max(dmax, d);
       }
     }
+    if (total) {
+      __syncwarp();
+      if (lane < static_cast<int>(kCwBatch)) {
+        fword |= sf[lane];
+        sf[lane] = 0;
+      }
+      __syncwarp();
+    }
+    ex += exb;
+    cnt += __popc(fword);
     if (wl < wend) {
       nb[wl] = fword;
       if (fword) op.dense_word(wl, fword);
     }
   }
-  if (heavy && __any_sync(0xffffffffu, big) && lane == 0) *heavy = 1u;
+  if (heavy && __any_sync(0xffffffffu, dmax > kBitmapPushMaxDeg) && lane == 0) *heavy = 1u;
   cnt = warp_sum(cnt);
   degsum = warp_sum(degsum);
   if (lane == 0 && cnt) atomicAdd(packed, (static_cast<unsigned long long>(cnt) << kPackShift) | degsum);
@@ -695,15 +719,8 @@ __device__ GBG_PB_INLINE void push_bitmap(G g, const uint32_t* fbm, uint64_t nwo
     for (uint32_t r0 = 0; r0 < total; r0 += 32) {
       const uint32_t t = r0 + lane;
       const bool c = t < total;
-      uint32_t j = 0, ej = 0;
-#pragma unroll
-      for (uint32_t k = 0; k < kPushBatch; ++k) {
-        const uint32_t ek = __shfl_sync(0xffffffffu, excl, k);
-        if (k < B && ek <= t) {
-          j = k;
-          ej = ek;
-        }
-      }
+      const uint32_t j = packed_word<kPushBatch>(excl, t);
+      const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
       const uint32_t fwj = __shfl_sync(0xffffffffu, fw, j);
       const uint32_t u = c ? static_cast<uint32_t>((wb + j) * 32 + __fns(fwj, 0, static_cast<int>(t - ej + 1))) : 0u;
       uint64_t b = 0;
