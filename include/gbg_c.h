@@ -190,6 +190,10 @@ gbg_status gbg_edge_map(gbg_graph* g, const uint32_t* ids, uint64_t k, const uin
 /* gb::bfs (algorithms.cpp:29-58), direction-optimising with the reference
  * switch; depth int32[n], -1 = unreached (kInfiniteDistance). */
 gbg_status gbg_bfs(gbg_graph* g, uint32_t source, int32_t* depth, gbg_bfs_stats* stats);
+/* gbg_bfs_device: depths stay in device memory.  With stats == NULL nothing
+ * returns to the host and the call is asynchronous on the handle's stream
+ * (gbg_stream(); gbg_synchronize() or stream-ordered work before reading
+ * depth_dev); with stats the call synchronises to fill them. */
 gbg_status gbg_bfs_device(gbg_graph* g, uint32_t source, int32_t* depth_dev, gbg_bfs_stats* stats);
 /* gb::pagerank (algorithms.cpp:508-555): fp64, uniform dangling
  * redistribution, stop at max_iters or L1 step < tolerance.  damping must be

@@ -419,12 +419,15 @@ bool bfs_coop(gbg_graph* g, G view, uint32_t src, int32_t* depth, gbg_bfs_stats*
   GBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bfs_coop_k<G>), grid, kPushThreads, args, 0,
                                        g->stream));
   g->launches++;
+  // no statistics wanted: nothing comes back to the host, so the call is
+  // asynchronous on the handle's stream (one launch, no readback or sync)
+  if (!st) return true;
   GBG_CUDA(cudaMemcpyAsync(g->hscalar, stat, kStatWords * sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
   GBG_CUDA(cudaStreamSynchronize(g->stream));
   const uint64_t* hs = g->hscalar;
   const unsigned long long* hx = reinterpret_cast<const unsigned long long*>(hs + 2 * ML + 4);
   const int32_t* hm = reinterpret_cast<const int32_t*>(hs + 3 * ML + 4);
-  if (st) {
+  {
     std::memset(st, 0, sizeof(*st));
     const uint64_t levels = hs[2 * GBG_MAX_LEVELS + 2];
     st->levels = levels;

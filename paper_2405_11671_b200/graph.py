@@ -466,7 +466,13 @@ def bfs(g: _Graph, source: int) -> BfsResult:
     return BfsResult(depth=depth, **_stats(st))
 
 
-def bfs_device(g: _Graph, source: int, depth_ptr: int) -> dict:
+def bfs_device(g: _Graph, source: int, depth_ptr: int, stats: bool = True):
+    """gbg_bfs_device: depths stay on the device.  stats=False passes NULL
+    statistics: the call is then asynchronous on the handle's stream
+    (nothing returns to the host) and the result is None."""
+    if not stats:
+        _check(_L.gbg_bfs_device(g.handle, source, depth_ptr, None))
+        return None
     st = BfsStats()
     _check(_L.gbg_bfs_device(g.handle, source, depth_ptr, C.byref(st)))
     return _stats(st)

@@ -25,8 +25,15 @@ for S in [int(x) for x in (sys.argv[1:] or ["16", "24"])]:
         st = gbg.bfs_device(g, src, depth.data_ptr())
     e1.record(s)
     e1.synchronize()
+    ts = e0.elapsed_time(e1) / 10
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(10):
+        gbg.bfs_device(g, src, depth.data_ptr(), stats=False)  # NULL stats: asynchronous
+    e1.record(s)
+    e1.synchronize()
     os.environ["GBG_BFS_LEVEL_TIMES"] = "1"  # one untimed, instrumented call
     st = gbg.bfs_device(g, src, depth.data_ptr())
     os.environ.pop("GBG_BFS_LEVEL_TIMES")
-    print(f"s{S}: bfs {e0.elapsed_time(e1) / 10:.3f} ms levels {st['modes']} level_ms "
+    print(f"s{S}: bfs {e0.elapsed_time(e1) / 10:.3f} ms (with stats {ts:.3f}) levels {st['modes']} level_ms "
           f"{[round(x, 4) for x in st['level_ms']]}", flush=True)

@@ -268,6 +268,14 @@ def test_rmat_generator_and_bfs_cc_match_golden(gbg, S):
     assert digest(r.depth) == gd["bfs"]["digest"]
     assert r.modes == gd["bfs"]["modes"] and r.frontier_sizes == gd["bfs"]["frontier_sizes"]
     assert r.reached == gd["bfs"]["reached"]
+    # NULL statistics: asynchronous on the handle's stream, queued twice
+    # back to back into one device buffer; same depths after a synchronise
+    import torch
+    dd = torch.full((g.num_vertices(),), 7, dtype=torch.int32, device="cuda")
+    assert gbg.bfs_device(g, src, dd.data_ptr(), stats=False) is None
+    assert gbg.bfs_device(g, src, dd.data_ptr(), stats=False) is None
+    g.synchronize()
+    assert digest(dd.cpu().numpy()) == gd["bfs"]["digest"]
     assert digest(gbg.cc(g)) == gd["cc"]["digest"]
     assert gbg.triangle_count(g) == gd["tc"]["triangles"]
 
