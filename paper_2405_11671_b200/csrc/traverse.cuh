@@ -442,45 +442,51 @@ __device__ __forceinline__ void packed_bit(uint32_t w, uint32_t excl, uint32_t t
 // per-batch bases replace 64-bit index arithmetic per word.  The owning
 // warp writes the output word and publishes the visited bits.
 template <class G, class Op>
-__device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords,
+__device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, uint32_t* nb, uint64_t nwords64,
                                               unsigned long long* packed, const uint64_t* fd,
                                               unsigned long long* examined, unsigned* heavy) {
-  __shared__ uint32_t s_fw[32][kCwBatch];  // found bits of the packed rounds, per warp and batch word
+  constexpr int kWarps = (kPullThreads > kPushThreads ? kPullThreads : kPushThreads) / 32;  // callers' CTA sizes
+  __shared__ uint32_t s_fw[kWarps][kCwBatch];       // found bits of the packed rounds, per warp and batch word
+  __shared__ uint8_t s_miss[kWarps][kCwBatch * 32];  // phase-1 misses of a batch in order: word << 5 | bit
   const int lane = threadIdx.x & 31;
   const uint32_t lbit = 1u << lane;
   uint32_t* sf = s_fw[threadIdx.x >> 5];
-  const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint8_t* sm = s_miss[threadIdx.x >> 5];
+  // word indices fit 32 bits (ids are uint32: at most 2^27 words)
+  const uint32_t nwords = static_cast<uint32_t>(nwords64);
+  const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t tail = (g.n & 31) ? (1u << (g.n & 31)) - 1u : 0xffffffffu;  // live bits of the last word
   // strided batches of B words (B <= kCwBatch): a warp's batches spread
   // over the whole id range, which balances the per-word work (static
   // contiguous runs left a 10-40 us tail of late CTAs before the barrier;
   // a shared batch counter costs more in contention than it recovers)
-  const uint64_t per = (nwords + nwarps - 1) / nwarps;
-  const uint32_t B = static_cast<uint32_t>(per < kCwBatch ? (per ? per : 1) : kCwBatch);
+  const uint32_t per = (nwords + nwarps - 1) / nwarps;
+  const uint32_t B = per < kCwBatch ? (per ? per : 1) : static_cast<uint32_t>(kCwBatch);
+  const uint64_t stride = static_cast<uint64_t>(nwarps) * B;
   unsigned long long cnt = 0, degsum = 0, ex = 0;
   uint32_t dmax = 0;
   if (lane < static_cast<int>(kCwBatch)) sf[lane] = 0;
   __syncwarp();
-  for (uint64_t wb = gwarp * B; wb < nwords; wb += nwarps * B) {
-    const uint64_t wend = wb + B < nwords ? wb + B : nwords;
-    const uint64_t wl = wb + lane;
+  for (uint64_t wb64 = static_cast<uint64_t>(gwarp) * B; wb64 < nwords; wb64 += stride) {
+    const uint32_t wb = static_cast<uint32_t>(wb64);
+    const uint32_t wl = wb + lane;
+    const bool mine = lane < static_cast<int>(B) && wl < nwords;
     uint32_t cw = 0;  // lanes past the batch keep 0: their words have no live vertex
-    if (wl < wend) {
+    if (mine) {
       cw = op.cond_word(wl);
-      if (wl * 32 + 32 > g.n) cw &= g.n > wl * 32 ? (1u << (g.n - wl * 32)) - 1u : 0u;
+      if (wl == nwords - 1) cw &= tail;
     }
-    uint32_t pc = __popc(cw);
-    uint32_t excl = warp_inclusive_scan(pc) - pc;
-    uint32_t total = __shfl_sync(0xffffffffu, excl + pc, 31);
     uint32_t fword = 0;  // lane k < B: found bits of word wb + k
-    uint32_t todo = cw;  // lane k < B: live bits of word wb + k still to resolve
     uint32_t exb = 0;
-    bool first_done = false;
+    const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(cw));
+    const uint32_t v0 = wb * 32;
+    bool rounds = total != 0;
     if (total > 32) {
-      // phase 1: first-neighbour tests, 4 words at a time
-      const uint32_t v0 = static_cast<uint32_t>(wb * 32) + lane;
-      const uint64_t* fdl = fd + wb * 32 + lane;
-      uint32_t miss = 0;
+      // phase 1: first-neighbour tests, 4 words at a time; the misses go
+      // to the warp's shared list in (word, bit) order
+      const uint64_t* fdl = fd + static_cast<uint64_t>(wb) * 32 + lane;
+      uint32_t nmiss = 0;
 #pragma unroll
       for (uint32_t k0 = 0; k0 < kCwBatch; k0 += kPh1) {
         if (k0 >= B) break;
@@ -497,7 +503,7 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
 #pragma unroll
         for (uint32_t q = 0; q < kPh1; ++q) {
           const uint32_t d = fd_deg(x[q]);  // 0 for a lane without a live vertex
-          if (h[q] && !op.update(fd_first(x[q]), v0 + (k0 + q) * 32)) h[q] = false;
+          if (h[q] && !op.update(fd_first(x[q]), v0 + (k0 + q) * 32 + lane)) h[q] = false;
           exb += d ? 1 : 0;
           if (h[q]) {
             degsum += d;
@@ -505,36 +511,40 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
           }
           const uint32_t fm = __ballot_sync(0xffffffffu, h[q]);
           const uint32_t mm = __ballot_sync(0xffffffffu, !h[q] && d > 1);
-          if (lane == static_cast<int>(k0 + q)) {
-            fword = fm;
-            miss = mm;
-          }
+          if (lane == static_cast<int>(k0 + q)) fword = fm;
+          if (mm & lbit) sm[nmiss + __popc(mm & (lbit - 1u))] = static_cast<uint8_t>((k0 + q) * 32 + lane);
+          nmiss += __popc(mm);
         }
       }
-      todo = miss;
-      pc = __popc(todo);
-      excl = warp_inclusive_scan(pc) - pc;
-      total = __shfl_sync(0xffffffffu, excl + pc, 31);
-      first_done = true;
-    }
-    // packed rounds over the remaining live vertices
-    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
-      const uint32_t t = r0 + lane;
-      const bool c = t < total;
+      __syncwarp();
+      for (uint32_t r0 = 0; r0 < nmiss; r0 += 32) {
+        const uint32_t t = r0 + lane;
+        const bool c = t < nmiss;
+        const uint32_t pos = c ? sm[t] : 0u;
+        uint32_t d;
+        if (pull_vertex<false>(g, fb, op, fd, c, v0 + pos, d, ex)) {
+          atomicOr(sf + (pos >> 5), 1u << (pos & 31));
+          degsum += d;
+          dmax = max(dmax, d);
+        }
+      }
+      rounds = nmiss != 0;
+    } else if (total) {
+      // at most 32 live vertices: one packed round, first neighbours included
+      const uint32_t pc = __popc(cw);
+      const uint32_t excl = warp_inclusive_scan(pc) - pc;
+      const bool c = static_cast<uint32_t>(lane) < total;
       uint32_t j, bit;
-      packed_bit<kCwBatch>(todo, excl, t, j, bit);
+      packed_bit<kCwBatch>(cw, excl, lane, j, bit);
       if (!c) bit = 0;
-      const uint32_t v = static_cast<uint32_t>((wb + j) * 32 + bit);
       uint32_t d;
-      const bool found = first_done ? pull_vertex<false>(g, fb, op, fd, c, v, d, ex)
-                                    : pull_vertex<true>(g, fb, op, fd, c, v, d, ex);
-      if (found) {
+      if (pull_vertex<true>(g, fb, op, fd, c, v0 + j * 32 + bit, d, ex)) {
         atomicOr(sf + j, 1u << bit);
         degsum += d;
         dmax = max(dmax, d);
       }
     }
-    if (total) {
+    if (rounds) {
       __syncwarp();
       if (lane < static_cast<int>(kCwBatch)) {
         fword |= sf[lane];
@@ -544,7 +554,7 @@ __device__ __forceinline__ void pull_words_cw(G g, const uint32_t* fb, Op op, ui
     }
     ex += exb;
     cnt += __popc(fword);
-    if (wl < wend) {
+    if (mine) {
       nb[wl] = fword;
       if (fword) op.dense_word(wl, fword);
     }
