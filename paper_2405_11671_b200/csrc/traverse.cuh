@@ -740,14 +740,22 @@ __device__ GBG_PB_INLINE void push_bitmap(G g, const uint32_t* fbm, uint64_t nwo
       uint32_t steps = ds;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
-      for (uint32_t k = 0; k < steps; ++k) {
-        uint32_t v = 0;
-        bool emit = false;
-        if (k < ds) {
-          v = g.at(b + k);
-          emit = op.cond(v) && op.claim(v) && op.update(u, v);
+      // four list entries and then their cond tests in flight at once: a
+      // round is one dependent chain per warp (bitmap word -> row bounds ->
+      // entries -> cond), and the level has only a few rounds per warp
+      for (uint32_t k0 = 0; k0 < steps; k0 += 4) {
+        uint32_t v[4];
+        bool ok[4];
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) v[q] = k0 + q < ds ? g.at(b + k0 + q) : 0u;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) ok[q] = k0 + q < ds && op.cond(v[q]);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          if (k0 + q >= steps) break;
+          const bool emit = ok[q] && op.claim(v[q]) && op.update(u, v[q]);
+          emit_warp(g, emit, v[q], out, out_dscan, out_bm, packed);
         }
-        emit_warp(g, emit, v, out, out_dscan, out_bm, packed);
       }
       uint32_t hard = __ballot_sync(0xffffffffu, d > kPullSerial);
       while (hard) {
