@@ -209,6 +209,34 @@ def test_bfs_known_answers(gbg, orc):
 
 
 @pytest.mark.parametrize("kind", ["csr", "blocked"])
+def test_bfs_unreached_depths(gbg, orc, kind):
+    """Unreached vertices read -1 whatever the level pattern and whatever
+    the device buffer held before: an isolated source on a tiny graph
+    (level 1 dense: 1 > m / 20), a path (never dense), a star (level 1
+    dense), with isolated and unreachable vertices in every case."""
+    import torch
+    cases = []
+    n, pairs = undirected(40, [(1, 2), (2, 3), (5, 6)], orc)            # source 0 isolated, m = 6
+    cases.append((n, pairs, 0))
+    n, pairs = undirected(300, [(i, i + 1) for i in range(200)] + [(250, 251)], orc)  # path + far component
+    cases.append((n, pairs, 0))
+    n, pairs = undirected(600, [(0, i) for i in range(1, 400)] + [(450, 451)], orc)   # star
+    cases.append((n, pairs, 0))
+    cases.append((n, pairs, 450))
+    cases.append((n, pairs, 599))                                          # isolated source, larger graph
+    for n, pairs, src in cases:
+        off, nbr = csr(n, pairs)
+        g = gbg.CsrGraph.build(n, pairs) if kind == "csr" else gbg.BlockedGraph.build(n, pairs)
+        d, modes, sizes = orc.bfs(n, off, nbr, src)
+        r = gbg.bfs(g, src)
+        assert np.array_equal(r.depth, d) and r.modes == modes and r.frontier_sizes == sizes
+        dd = torch.full((n,), 123456, dtype=torch.int32, device="cuda")
+        gbg.bfs_device(g, src, dd.data_ptr(), stats=False)
+        g.synchronize()
+        assert np.array_equal(dd.cpu().numpy(), d)
+
+
+@pytest.mark.parametrize("kind", ["csr", "blocked"])
 def test_bfs_matches_oracle_seeded(gbg, ref, orc, kind):
     for trial in range(20):
         n, pairs = ref.er(150 + 37 * trial, 0.03, 100 + trial)
