@@ -113,6 +113,9 @@ struct BitsToIdsDscanOut {
 constexpr int kPushThreads = 256;
 constexpr int kPushIPT = 8;
 constexpr int kPushTile = kPushThreads * kPushIPT;
+// edge count of a push from which emissions are aggregated per CTA (one
+// atomic per CTA and step) instead of per warp
+constexpr uint64_t kPushCtaAggregate = 1ull << 16;
 
 template <class G>
 struct FrontierDegIn {
@@ -217,6 +220,7 @@ __device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, c
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  __shared__ unsigned long long s_agg[kPushThreads / 32];
   for (uint32_t base = 0; base < len; base += kPushThreads) {
     const uint32_t k = base + threadIdx.x;
     bool emit = false;
@@ -230,22 +234,55 @@ __device__ __forceinline__ void push_tile(G g, const uint32_t* F, uint32_t nf, c
       v = g.at(b + (e0 + k - dscan[i]));
       emit = op.cond(v) && op.claim(v) && op.update(u, v);
     }
-    const uint32_t mask = __ballot_sync(0xffffffffu, emit);
-    if (mask) {
-      const uint64_t dv = emit ? g.degree(v) : 0;
-      const uint64_t dinc = warp_inclusive_scan(dv);
-      const uint64_t dtot = __shfl_sync(0xffffffffu, dinc, 31);
-      const int leader = __ffs(mask) - 1;
-      uint64_t old = 0;
-      if (lane == leader)
-        old = atomicAdd(packed, (static_cast<unsigned long long>(__popc(mask)) << kPackShift) | dtot);
-      old = __shfl_sync(0xffffffffu, old, leader);
-      if (emit) {
-        const uint64_t pos = pack_count(old) + __popc(mask & ((1u << lane) - 1));
-        out[pos] = v;
-        if (out_dscan) out_dscan[pos] = pack_degsum(old) + dinc - dv;
-        if (out_bm) atomicOr(out_bm + (v >> 5), 1u << (v & 31));
+    if (E < kPushCtaAggregate) {
+      // small levels: one warp-aggregated atomic per warp and step
+      const uint32_t mask = __ballot_sync(0xffffffffu, emit);
+      if (mask) {
+        const uint64_t dv = emit ? g.degree(v) : 0;
+        const uint64_t dinc = warp_inclusive_scan(dv);
+        const uint64_t dtot = __shfl_sync(0xffffffffu, dinc, 31);
+        const int leader = __ffs(mask) - 1;
+        uint64_t old = 0;
+        if (lane == leader)
+          old = atomicAdd(packed, (static_cast<unsigned long long>(__popc(mask)) << kPackShift) | dtot);
+        old = __shfl_sync(0xffffffffu, old, leader);
+        if (emit) {
+          const uint64_t pos = pack_count(old) + __popc(mask & ((1u << lane) - 1));
+          out[pos] = v;
+          if (out_dscan) out_dscan[pos] = pack_degsum(old) + dinc - dv;
+          if (out_bm) atomicOr(out_bm + (v >> 5), 1u << (v & 31));
+        }
       }
+      continue;
+    }
+    // large levels: one atomic on the packed (count, degree sum) counter
+    // per CTA and step.  The counter is one address, and a level that emits
+    // most of its edges (the push from a hub: 406 K emissions at scale 24
+    // level 0) was bound by the rate of same-address atomics (27 -> 21 us)
+    if (!__syncthreads_or(emit)) continue;  // also orders the previous step's s_agg reads before this step's writes
+    const uint32_t mask = __ballot_sync(0xffffffffu, emit);
+    const uint64_t dv = emit ? g.degree(v) : 0;
+    const uint64_t dinc = warp_inclusive_scan(dv);
+    const uint64_t dtot = __shfl_sync(0xffffffffu, dinc, 31);
+    const int warp = threadIdx.x >> 5;
+    if (lane == 0) s_agg[warp] = (static_cast<unsigned long long>(__popc(mask)) << kPackShift) | dtot;
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned long long mine = lane < kPushThreads / 32 ? s_agg[lane] : 0ull;
+      const unsigned long long inc = warp_inclusive_scan(mine);
+      const unsigned long long tot = __shfl_sync(0xffffffffu, inc, 31);
+      unsigned long long old = 0;
+      if (lane == 0 && tot) old = atomicAdd(packed, tot);
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (lane < kPushThreads / 32) s_agg[lane] = old + inc - mine;
+    }
+    __syncthreads();
+    if (emit) {
+      const unsigned long long old = s_agg[warp];
+      const uint64_t pos = pack_count(old) + __popc(mask & ((1u << lane) - 1));
+      out[pos] = v;
+      if (out_dscan) out_dscan[pos] = pack_degsum(old) + dinc - dv;
+      if (out_bm) atomicOr(out_bm + (v >> 5), 1u << (v & 31));
     }
   }
 }
