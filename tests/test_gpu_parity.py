@@ -236,6 +236,28 @@ def test_bfs_unreached_depths(gbg, orc, kind):
         assert np.array_equal(dd.cpu().numpy(), d)
 
 
+def test_bfs_large_sparse_push_matches_oracle(gbg, orc):
+    """A sparse level of >= 64 K edges (emissions aggregated per CTA): a hub
+    with 80,000 leaves inside enough filler edges that m / 20 stays above
+    the hub's degree, so level 1 is a push of 80,000 edges that emits all
+    of them; levels, sizes and depths against the oracle."""
+    hub = 80000
+    fill = 800000
+    e = np.empty((hub + fill, 2), dtype=np.uint32)
+    e[:hub, 0] = 0
+    e[:hub, 1] = np.arange(1, hub + 1, dtype=np.uint32)
+    base = hub + 1
+    e[hub:, 0] = base + 2 * np.arange(fill, dtype=np.uint32)
+    e[hub:, 1] = e[hub:, 0] + 1
+    n, pairs = orc.normalize(e, base + 2 * fill)
+    off, nbr = csr(n, pairs)
+    d, modes, sizes = orc.bfs(n, off, nbr, 0)
+    assert modes[0] == 0 and sizes[1] == hub  # level 1 really is the large sparse push
+    r = gbg.bfs(gbg.CsrGraph.build(n, pairs), 0)
+    assert np.array_equal(r.depth, d) and r.modes == modes and r.frontier_sizes == sizes
+    assert r.degree_sums[1] == hub  # every leaf emitted once, with its degree
+
+
 @pytest.mark.parametrize("kind", ["csr", "blocked"])
 def test_bfs_matches_oracle_seeded(gbg, ref, orc, kind):
     for trial in range(20):
